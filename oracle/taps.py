@@ -1,0 +1,101 @@
+"""Oracle: exact tap-offset tables and angle assignment.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  It shares no code
+with the CUDA path (paper_2309_15812_b200/).
+
+What it computes:
+  * Def. 1, Eq. "coordinate" and Appendix Eq. coordinate1d:
+        oh_k = floor( -(k - pad) * sin(theta) ),   ow_k = floor( (k - pad) * cos(theta) )
+    the floor of the EXACT real value (reading R3).
+  * Direction groups: D angles i*180/D, channels split into D equal groups.
+
+Exactness: the angle is a binary double, i.e. a rational number of degrees.  By
+Niven's theorem sin(t deg) for rational t is rational only when it is 0, +-1/2 or
++-1 (t = 0, 30, 90, 150, 180, 210, 270, 330 mod 360), and likewise cos (t = 0, 60,
+90, 120, 180, 240, 270, 300).  Those cases are evaluated in exact rational
+arithmetic (fractions.Fraction).  Otherwise m*sin(t) (m != 0 integer) is
+irrational, so it is never an integer, and its floor is evaluated with mpmath at
+80 significant digits; the distance to the nearest integer is asserted to be far
+above the evaluation error, so the floor is exact.
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import mpmath
+
+_DPS = 80
+
+# Niven's theorem tables (degrees mod 360 -> exact rational value)
+_SIN_RATIONAL = {0: Fraction(0), 30: Fraction(1, 2), 90: Fraction(1), 150: Fraction(1, 2),
+                 180: Fraction(0), 210: Fraction(-1, 2), 270: Fraction(-1), 330: Fraction(-1, 2)}
+_COS_RATIONAL = {0: Fraction(1), 60: Fraction(1, 2), 90: Fraction(0), 120: Fraction(-1, 2),
+                 180: Fraction(-1), 240: Fraction(-1, 2), 270: Fraction(0), 300: Fraction(1, 2)}
+
+
+def _reduce_deg(theta_deg: float) -> Fraction:
+    return Fraction(theta_deg) % 360
+
+
+def _exact_floor_times(m: int, t: Fraction, fn: str) -> int:
+    """floor(m * fn(t degrees)) exactly, fn in {"sin", "cos"}."""
+    if m == 0:
+        return 0
+    table = _SIN_RATIONAL if fn == "sin" else _COS_RATIONAL
+    if t.denominator == 1 and int(t) in table:
+        v = m * table[int(t)]
+        return v.numerator // v.denominator  # Fraction floor
+    with mpmath.workdps(_DPS):
+        tt = mpmath.mpf(t.numerator) / t.denominator
+        rad = tt * mpmath.pi / 180
+        v = m * (mpmath.sin(rad) if fn == "sin" else mpmath.cos(rad))
+        f = int(mpmath.floor(v))
+        dist = min(v - f, f + 1 - v)
+        # irrational (Niven) => not an integer; must be resolvable at this precision
+        assert dist > mpmath.mpf(10) ** (-(_DPS - 20)), (m, t, fn)
+    return f
+
+
+def taps_exact(K: int, pad: int, theta_deg: float):
+    """Exact tap table for one angle: list of (oh_k, ow_k), k = 0..K-1."""
+    t = _reduce_deg(theta_deg)
+    out = []
+    for k in range(K):
+        m = k - pad
+        oh = _exact_floor_times(-m, t, "sin")   # floor(-(k-pad) sin θ)
+        ow = _exact_floor_times(m, t, "cos")    # floor( (k-pad) cos θ)
+        out.append((oh, ow))
+    return out
+
+
+def taps_table(K: int, pad: int, angles_deg):
+    """Per-channel tables: (oh[C][K], ow[C][K]) as nested lists of int."""
+    cache = {}
+    oh, ow = [], []
+    for a in angles_deg:
+        key = float(a)
+        if key not in cache:
+            cache[key] = taps_exact(K, pad, key)
+        t = cache[key]
+        oh.append([p[0] for p in t])
+        ow.append([p[1] for p in t])
+    return oh, ow
+
+
+def direction_angles(D: int, C: int, assign: str = "contiguous", shift_deg: float = 0.0):
+    """Angle per channel (degrees): D angles i*180/D, channels in D equal
+    groups.  "contiguous": group of channel c is floor(c*D/C) (SPEC S:128 reading);
+    "cycled": group is c mod D (BASELINE.json configs[1] reading).  The D=C case
+    gives channel c the angle c*180/C under both readings.  shift_deg adds a
+    layer-wise rotation ("alternating 90 deg"), reduced mod 180."""
+    if D < 1 or C < 1 or (C % D != 0 and D != C):
+        raise ValueError("D must divide C (or D == C)")
+    out = []
+    for c in range(C):
+        g = (c * D) // C if assign == "contiguous" else c % D
+        a = Fraction(g * 180, D) + Fraction(shift_deg)
+        if shift_deg:
+            a = a % 180
+        out.append(float(a))
+    return out
