@@ -1,0 +1,344 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the oriented 1D depthwise conv training step on B200.
+
+A "step" = one pass of the whole hot path over one batch:
+forward (x -> y), backward_input (dy -> dx), backward_weight (x, dy -> dW), and,
+at N > 1 GPUs, the NCCL all-reduce of dW (row a8).  Workload = BASELINE.json
+configs[1], the ConvNeXt-T-1D stage-1 layer: N=64, C=96, 56x56, K=31, 8 angles
+cycled over channels; synthetic seeded inputs (paper_2309_15812_b200/inputs.py).
+
+metric/value: algorithmic HBM bytes of the step (each pass reads its inputs and
+writes its outputs once: 3 x 154.2 MB fp32) divided by the device time, summed
+over ranks (weak scaling: every rank runs the full configs[1] batch).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f32|bf16] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "oriented 1D dwconv fwd+bwd HBM GB/s vs peak; ConvNeXt-T-1D train imgs/s 1-8 GPU"
+PASSES = ("forward", "backward_input", "backward_weight")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--flags", type=int, default=0, help="o1d_desc.flags (1 = force generic kernels)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary bf16 measurement")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def algorithmic_bytes(wl, es):
+    """Bytes each pass must move: read inputs once, write outputs once."""
+    x = wl.N * wl.C * wl.H * wl.W * es
+    y = wl.N * wl.C * wl.H * wl.W * es  # P = H, Q = W at stride 1
+    wb = wl.C * wl.K * 4
+    return {"forward": x + wb + y, "backward_input": y + wb + x, "backward_weight": x + y + wb}
+
+
+def algorithmic_fmas(wl):
+    return wl.N * wl.C * wl.H * wl.W * wl.K  # dense taps per output (zero padding is free in smem)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [c.strip() for c in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_baseline(wl, dtype_name, target_s=12.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+    import numpy as np
+
+    import oracle
+    from oracle import taps as T
+    from paper_2309_15812_b200 import inputs
+
+    th = max(1, oracle.max_threads())
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    oh, ow = (np.array(a, np.int32) for a in T.taps_table(wl.K, wl.pad, angles))
+    n = max(1, wl.N // 8)
+    x = inputs.activation((n, wl.C, wl.H, wl.W), 0, dtype_name).astype(np.float64)
+    dy = inputs.activation((n, wl.C, wl.H, wl.W), 2, dtype_name).astype(np.float64)
+    w = inputs.weights(wl.C, wl.K, 1).astype(np.float64)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        oracle.forward(x, w, oh, ow, 1, th)
+        oracle.backward_input(dy, w, oh, ow, wl.H, wl.W, 1, th)
+        oracle.backward_weight(x, dy, oh, ow, 1, th)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= target_s or steps >= 200:
+            break
+    es = 4 if dtype_name == "f32" else 2
+    from dataclasses import replace
+    bytes_step = sum(algorithmic_bytes(replace(wl, N=n), es).values())
+    return {"value": bytes_step * steps / el / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle",
+            "sample": f"{steps} steps of the 3-pass layer step at N={n} (of {wl.N}), "
+                      f"C={wl.C}, {wl.H}x{wl.W}, K={wl.K}, f64 accumulation, {el:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on rank 0 only."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2309_15812_b200 import inputs
+    wl = inputs.S1
+    cb = cpu_baseline(wl, args.dtype, target_s=max(2.0, 60.0 / max(1, args.steps + args.warmup)))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64)",
+            "config": {"workload": wl.name, "N": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
+                       "angles": f"D={wl.D} {wl.assign}", "stride": 1},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_15812_b200 import binding as B
+    from paper_2309_15812_b200 import inputs
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.dtype]
+    es = 4 if args.dtype == "f32" else 2
+    wl = inputs.S1
+    angles = B.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, angles, dtype=tdt, flags=args.flags, device=dev)
+    # two rotating buffer sets so every pass streams from HBM (each set 4 x 77 MB > L2)
+    sets = []
+    for s in range(2):
+        x = torch.from_numpy(inputs.activation(plan.x_shape(), 0 + 10 * s, args.dtype)).to(dev, tdt)
+        dy = torch.from_numpy(inputs.activation(plan.y_shape(), 2 + 10 * s, args.dtype)).to(dev, tdt)
+        sets.append({"x": x, "dy": dy, "y": torch.empty_like(dy), "dx": torch.empty_like(x)})
+    w = torch.from_numpy(inputs.weights(wl.C, wl.K, 1)).to(dev)
+    dW = torch.empty_like(w)
+    ws = B.workspace(plan)
+    stream = torch.cuda.current_stream()
+
+    def step(i, ev=None):
+        b = sets[i & 1]
+        if ev is not None:
+            ev[0].record(stream)
+        B.forward(plan, b["x"], w, b["y"])
+        if ev is not None:
+            ev[1].record(stream)
+        B.backward_input(plan, b["dy"], w, b["dx"])
+        if ev is not None:
+            ev[2].record(stream)
+        B.backward_weight(plan, b["x"], b["dy"], dW, ws)
+        if ev is not None:
+            ev[3].record(stream)
+        if world > 1:
+            dist.all_reduce(dW)  # row a8: NCCL sum of the weight gradient over NVLink
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(i, evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    per_pass = {p: 0.0 for p in PASSES}
+    for e in evs:
+        for j, p in enumerate(PASSES):
+            per_pass[p] += e[j].elapsed_time(e[j + 1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ab = algorithmic_bytes(wl, es)
+    bytes_step = sum(ab.values())
+    value = bytes_step * args.steps * world / (max_ms * 1e-3) / 1e9
+    ms_step = max_ms / args.steps
+    peak, peak_src = measured_peaks()
+    dom = max(PASSES, key=lambda p: per_pass[p])
+    dom_ms = per_pass[dom] / args.steps
+    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    launches = sum(plan.launches_per_call(j) for j in range(3)) * args.steps
+
+    # end to end through the C ABI with pinned HOST buffers (H2D + 3 passes + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        xh = sets[0]["x"].cpu().pin_memory()
+        dyh = sets[0]["dy"].cpu().pin_memory()
+        wh = w.cpu().pin_memory()
+        yh, dxh, dWh = torch.empty_like(dyh).pin_memory(), torch.empty_like(xh).pin_memory(), torch.empty_like(wh).pin_memory()
+        dws = B.step_host_workspace(plan)
+        for _ in range(2):
+            B.step_host(plan, xh, wh, dyh, yh, dxh, dWh, dws)
+        n_e2e = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(n_e2e):
+            B.step_host(plan, xh, wh, dyh, yh, dxh, dWh, dws)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": bytes_step * n_e2e * world / (float(te.item()) * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size() + dyh.numel() * dyh.element_size()
+                                         + wh.numel() * 4),
+               "d2h_bytes_per_step": int(yh.numel() * yh.element_size() + dxh.numel() * dxh.element_size()
+                                         + dWh.numel() * 4),
+               "steps": n_e2e, "path": "o1d_step_host (pinned host buffers, one C-ABI call per step)"}
+
+    extra = {}
+    if rank == 0:
+        extra["per_pass_ms"] = {p: per_pass[p] / args.steps for p in PASSES}
+        extra["per_pass_gbs"] = {p: ab[p] / (per_pass[p] / args.steps * 1e-3) / 1e9 for p in PASSES}
+        extra["per_pass_frac_of_hbm"] = {p: extra["per_pass_gbs"][p] / peak for p in PASSES}
+        extra["fp32_tflops_dense"] = 3 * 2 * algorithmic_fmas(wl) / (ms_step * 1e-3) / 1e12
+        extra["imgs_per_s_layer_step"] = wl.N * world / (ms_step * 1e-3)
+        extra["plan"] = plan.describe()
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64 U[-1,1))",
+        "config": {"workload": wl.name, "N_per_gpu": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
+                   "angles": f"D={wl.D} {wl.assign}", "stride": 1, "layout": "NCHW",
+                   "parallelism": f"dp{world} (batch-sharded, NCCL all-reduce of dW)",
+                   "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ab[dom]},
+        "gpu_launches": launches, "clocks": ck, "e2e": e2e,
+    }
+    line.update(extra)
+    if rank == 0 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(wl, args.dtype)
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"error": repr(ex)}
+    if rank == 0 and not args.no_extra and args.dtype == "f32":
+        try:
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--dtype", "bf16", "--steps",
+                                  str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu",
+                                  "--no-extra", "--flags", str(args.flags)],
+                                 capture_output=True, text=True, timeout=600,
+                                 env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
+            b = json.loads(out.stdout.strip().splitlines()[-1])
+            line["bf16"] = {k: b[k] for k in ("value", "ms_per_step", "roofline", "per_pass_gbs",
+                                              "per_pass_frac_of_hbm")}
+        except Exception as ex:  # pragma: no cover
+            line["bf16"] = {"error": repr(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,165 @@
+/*
+ * oriented1d.h — C ABI of liboriented1d: the depthwise convolution of oriented
+ * 1D kernels (arXiv 2309.15812, "Convolutional Networks with Oriented 1D
+ * Kernels") on NVIDIA B200 (sm_100a).
+ *
+ * The operation (Def. 1):
+ *     y[n][c][p][q] = sum_{k=0}^{K-1} x[n][c][h][w] * w[c][k]
+ *     h = str*p + floor(-(k-pad) * sin(theta_c)),  w = str*q + floor((k-pad) * cos(theta_c))
+ * with zero padding outside [0,H) x [0,W) (reading R1), output size
+ * P = (H-1)/str + 1, Q = (W-1)/str + 1 (reading R2), floors of the exact real
+ * value (reading R3).  The paper writes x in R^{N x H x W x C} as INDEX
+ * notation; this library stores activations NCHW-contiguous (one plane per
+ * (n,c), row-major), see DESIGN.md §Layout.
+ *
+ * Conventions for every call:
+ *   - Every function returns o1d_status; nothing throws across the ABI.  On an
+ *     error, o1d_last_error() returns a thread-local, NUL-terminated message that
+ *     stays valid until the next call from the same thread.
+ *   - Argument validation is host-side and happens BEFORE any launch; a failing
+ *     call leaves every output untouched.
+ *   - Device pointers are caller-owned (PyTorch allocates them).  They must be
+ *     16-byte aligned, NCHW-contiguous, and must not alias each other.  The
+ *     library never allocates device memory except inside o1d_plan_create (the
+ *     plan's tap tables), and frees it in o1d_plan_destroy.
+ *   - Compute calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream).  Outputs are OVERWRITTEN, never accumulated into.
+ *   - Results are deterministic: the same plan and inputs give bitwise-identical
+ *     outputs (no floating-point atomics anywhere).
+ *   - Weights w and the weight gradient dW are fp32 [C][K] (k fastest).
+ *     Activations x, y, dy, dx have the plan's dtype (fp32, bf16 or fp16);
+ *     arithmetic is fp32 multiply-add with fp32 accumulation for every dtype.
+ *   - A plan is immutable after creation and may be used concurrently from
+ *     several host threads / streams.
+ */
+#ifndef ORIENTED1D_H_
+#define ORIENTED1D_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define O1D_API __attribute__((visibility("default")))
+#else
+#define O1D_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    O1D_OK = 0,
+    O1D_INVALID_ARG = 1,         /* NULL pointer / bad enum value                         */
+    O1D_INVALID_SHAPE = 2,       /* a dimension < 1                                       */
+    O1D_INVALID_CONFIG = 3,      /* K < 1, stride < 1, pad out of range, D does not divide C */
+    O1D_SHAPE_MISMATCH = 4,      /* buffer sizes disagree with the plan                   */
+    O1D_UNSUPPORTED = 5,         /* dtype / layout / shape the library does not implement */
+    O1D_MISALIGNED = 6,          /* a device pointer is not 16-byte aligned               */
+    O1D_WORKSPACE_TOO_SMALL = 7, /* ws_bytes < o1d_workspace_bytes(plan)                  */
+    O1D_CUDA_ERROR = 8,          /* a CUDA runtime / driver call failed                   */
+    O1D_JIT_ERROR = 9            /* runtime specialisation (NVRTC) failed                 */
+} o1d_status;
+
+typedef enum { O1D_F32 = 0, O1D_BF16 = 1, O1D_F16 = 2 } o1d_dtype;
+typedef enum { O1D_NCHW = 0 } o1d_layout;
+typedef enum { O1D_ASSIGN_CONTIGUOUS = 0, O1D_ASSIGN_CYCLED = 1 } o1d_assign;
+
+/* Problem descriptor (Def. 1): N batch, C channels, H x W input, K taps, stride
+ * `stride` on both axes, padding `pad` (pass -1 for the paper's default
+ * floor(K/2); otherwise 0 <= pad < K), activation dtype and layout.
+ * `flags` selects implementation options (O1D_FLAG_*), 0 = library default.  */
+typedef struct {
+    int32_t N, C, H, W, K;
+    int32_t stride;
+    int32_t pad;
+    int32_t dtype;   /* o1d_dtype  */
+    int32_t layout;  /* o1d_layout */
+    int32_t flags;
+} o1d_desc;
+
+/* Implementation selection (testing / tuning).  The default picks the fastest
+ * kernel family that supports the problem. */
+#define O1D_FLAG_FORCE_GENERIC 0x1  /* runtime-tap shared-memory kernels only (no JIT)  */
+#define O1D_FLAG_NO_TMA        0x2  /* stage tiles with plain loads instead of TMA      */
+
+typedef struct o1d_plan o1d_plan;
+
+/* Tap-offset table (Eq. coordinate, Eq. coordinate1d):
+ *   oh[c*K+k] = floor(-(k-pad) * sin(angles_deg[c])),  ow[c*K+k] = floor((k-pad) * cos(angles_deg[c]))
+ * evaluated as the floor of the exact real value (reading R3: f64 trig of the
+ * angle reduced mod 360 deg, snapped to the nearest integer when within 1e-9 of
+ * it).  angles_deg: host [C] (degrees, any real).  oh, ow: host [C][K] outputs.
+ * pad: -1 => floor(K/2).  Pure host function, no CUDA context needed. */
+O1D_API o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles_deg,
+                         int16_t *oh, int16_t *ow);
+
+/* Per-channel angles from D directions: angle_i = i*180/D deg,
+ * channels split into D equal groups; group(c) = floor(c*D/C) for
+ * O1D_ASSIGN_CONTIGUOUS, c mod D for O1D_ASSIGN_CYCLED; D == C gives
+ * c*180/C.  shift_deg != 0 adds the layer-wise rotation ("alternating
+ * 90 deg"), result reduced mod 180 deg.  out: host [C].  Errors:
+ * INVALID_CONFIG when D < 1 or (D does not divide C and D != C). */
+O1D_API o1d_status o1d_direction_angles(int32_t D, int32_t C, int32_t assign, double shift_deg, double *out);
+
+/* Create an immutable plan for descriptor `d` and per-channel angles
+ * angles_deg (host [C], degrees).  Computes the tap tables (as
+ * o1d_make_taps), de-duplicates equal tables, derives halo extents, selects
+ * (and, unless O1D_FLAG_FORCE_GENERIC, JIT-specialises) the kernels and uploads
+ * the tables to the current CUDA device.  *out receives the plan (NULL on
+ * error).  Must be called with the target device current. */
+O1D_API o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan **out);
+
+/* Output size: P = (H-1)/stride + 1, Q = (W-1)/stride + 1. */
+O1D_API o1d_status o1d_plan_out_shape(const o1d_plan *plan, int32_t *P, int32_t *Q);
+
+/* Copy the plan's tap table to host oh, ow [C][K]. */
+O1D_API o1d_status o1d_plan_get_taps(const o1d_plan *plan, int16_t *oh, int16_t *ow);
+
+/* Short NUL-terminated description of the kernels the plan selected
+ * (family, tile shape, number of specialised tap tables). */
+O1D_API const char *o1d_plan_describe(const o1d_plan *plan);
+
+/* Bytes of device workspace o1d_backward_weight needs (fp32 partial sums). */
+O1D_API size_t o1d_workspace_bytes(const o1d_plan *plan);
+
+/* Forward (Def. 1).  x: device [N][C][H][W] (plan dtype), w: device fp32
+ * [C][K], y: device [N][C][P][Q] (plan dtype), overwritten. */
+O1D_API o1d_status o1d_forward(const o1d_plan *plan, const void *x, const float *w, void *y, void *stream);
+
+/* backward_input: dx = adjoint of the forward map in x applied to dy
+ *   dx[n][c][h][w] = sum_k sum_{p,q : str*p+oh_ck = h, str*q+ow_ck = w} dy[n][c][p][q] * w[c][k]
+ * (reading A5).  dy: device [N][C][P][Q], w: device fp32 [C][K],
+ * dx: device [N][C][H][W], overwritten. */
+O1D_API o1d_status o1d_backward_input(const o1d_plan *plan, const void *dy, const float *w, void *dx, void *stream);
+
+/* backward_weight: dW[c][k] = sum_{n,p,q} dy[n][c][p][q] * x[n][c][str*p+oh_ck][str*q+ow_ck]
+ * (adjoint in w; out-of-range taps contribute 0).  x: device [N][C][H][W],
+ * dy: device [N][C][P][Q], dW: device fp32 [C][K] (overwritten, never
+ * accumulated), ws: device workspace of ws_bytes >= o1d_workspace_bytes(plan).
+ * Deterministic: partial sums are reduced in a fixed order. */
+O1D_API o1d_status o1d_backward_weight(const o1d_plan *plan, const void *x, const void *dy, float *dW,
+                               void *ws, size_t ws_bytes, void *stream);
+
+/* One training step of the layer through HOST buffers (the end-to-end path):
+ * copies x, w, dy host->device, runs forward, backward_input and
+ * backward_weight, copies y, dx, dW device->host, all on `stream`, then
+ * synchronises the stream.  Host buffers should be pinned for asynchronous
+ * copies.  dev_ws: device scratch of >= o1d_step_host_workspace_bytes(plan)
+ * bytes (holds device copies of every tensor and the dW workspace). */
+O1D_API size_t o1d_step_host_workspace_bytes(const o1d_plan *plan);
+O1D_API o1d_status o1d_step_host(const o1d_plan *plan, const void *x_h, const float *w_h, const void *dy_h,
+                         void *y_h, void *dx_h, float *dW_h, void *dev_ws, size_t dev_ws_bytes,
+                         void *stream);
+
+/* Number of kernel launches one call of each pass issues (for launch accounting). */
+O1D_API int32_t o1d_launches_per_call(const o1d_plan *plan, int32_t pass /* 0 fwd, 1 bwd_in, 2 bwd_w */);
+
+O1D_API void o1d_plan_destroy(o1d_plan *plan);
+O1D_API const char *o1d_last_error(void);
+O1D_API const char *o1d_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORIENTED1D_H_ */

@@ -1,0 +1,314 @@
+// o1d_generic.cu — runtime-tap ("generic") kernels of liboriented1d.
+//
+// These kernels take the tap table at run time, so they serve every plan
+// (arbitrary per-channel angles, any K, any stride).  They stage the input band
+// plus the angle-dependent halo in shared memory once (zero-filled outside the
+// image: reading R1), so every tap read is a shared-memory read — the paper's
+// "load the whole input in shared GPU memory ... cut the image into bands"
+// — but they get no register reuse across taps.  The JIT-specialised
+// kernels (o1d_spec_*.cuh) are the fast path; these are the fallback.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "o1d_internal.h"
+
+namespace o1d {
+namespace {
+
+template <typename T> __device__ __forceinline__ float ld_act(const T *p);
+template <> __device__ __forceinline__ float ld_act<float>(const float *p) { return __ldg(p); }
+template <> __device__ __forceinline__ float ld_act<__nv_bfloat16>(const __nv_bfloat16 *p) {
+    return __bfloat162float(*p);
+}
+template <> __device__ __forceinline__ float ld_act<__half>(const __half *p) { return __half2float(*p); }
+
+template <typename T> __device__ __forceinline__ T to_act(float v);
+template <> __device__ __forceinline__ float to_act<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_act<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ __half to_act<__half>(float v) { return __float2half_rn(v); }
+
+constexpr int kThreads = 256;
+constexpr int kSmemBudget = 96 * 1024;
+
+struct StencilArgs {
+    const void *in;
+    const float *w;
+    void *out;
+    const int16_t *dh, *dw;
+    int C, Hi, Wi, Ho, Wo, str, K;
+    int minDH, maxDH, minDW;
+    int band, bands;
+    int tileRows, tileCols, pitch;
+};
+
+// out[p][q] = sum_k in[str*p + dh_k][str*q + dw_k] * w_k, one CTA per (plane, band of output rows)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a) {
+    extern __shared__ float sm[];
+    const int tid = threadIdx.x;
+    const int plane = blockIdx.x / a.bands;
+    const int bnd = blockIdx.x - plane * a.bands;
+    const int c = plane % a.C;
+    const int p0 = bnd * a.band;
+    const int nrows = min(a.band, a.Ho - p0);
+    float *tile = sm;
+    int *toff = reinterpret_cast<int *>(tile + a.tileRows * a.pitch + 8 * a.str + a.pitch);
+    float *wk = reinterpret_cast<float *>(toff + a.K);
+    for (int k = tid; k < a.K; k += blockDim.x) {
+        toff[k] = (a.dh[c * a.K + k] - a.minDH) * a.pitch + (a.dw[c * a.K + k] - a.minDW);
+        wk[k] = a.w[c * a.K + k];
+    }
+    const T *in = static_cast<const T *>(a.in) + (size_t)plane * a.Hi * a.Wi;
+    const int h0 = a.str * p0 + a.minDH;
+    const int rows = a.str * (nrows - 1) + 1 + (a.maxDH - a.minDH);
+    for (int i = tid; i < rows * a.tileCols; i += blockDim.x) {
+        const int r = i / a.tileCols, j = i - r * a.tileCols;
+        const int h = h0 + r, v = a.minDW + j;
+        tile[r * a.pitch + j] = (h >= 0 && h < a.Hi && v >= 0 && v < a.Wi) ? ld_act<T>(in + (size_t)h * a.Wi + v) : 0.f;
+    }
+    __syncthreads();
+    T *out = static_cast<T *>(a.out) + (size_t)plane * a.Ho * a.Wo;
+    const int qg = (a.Wo + 3) >> 2;
+    for (int g = tid; g < nrows * qg; g += blockDim.x) {
+        const int pr = g / qg, q0 = (g - pr * qg) * 4;
+        const float *base = tile + pr * a.str * a.pitch + q0 * a.str;
+        float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+        for (int k = 0; k < a.K; ++k) {
+            const float *s = base + toff[k];
+            const float wv = wk[k];
+            acc0 = fmaf(s[0], wv, acc0);
+            acc1 = fmaf(s[a.str], wv, acc1);
+            acc2 = fmaf(s[2 * a.str], wv, acc2);
+            acc3 = fmaf(s[3 * a.str], wv, acc3);
+        }
+        T *o = out + (size_t)(p0 + pr) * a.Wo + q0;
+        o[0] = to_act<T>(acc0);
+        if (q0 + 1 < a.Wo) o[1] = to_act<T>(acc1);
+        if (q0 + 2 < a.Wo) o[2] = to_act<T>(acc2);
+        if (q0 + 3 < a.Wo) o[3] = to_act<T>(acc3);
+    }
+}
+
+// dx[h][w] = sum_k [str | h-oh_k, str | w-ow_k, in range] dy[(h-oh_k)/str][(w-ow_k)/str] * w_k
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_input_strided_kernel(const T *dy, const float *w, T *dx,
+                                                                     const int16_t *oh, const int16_t *ow,
+                                                                     int C, int H, int W, int P, int Q, int K,
+                                                                     int str, long total) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int v = (int)(i % W);
+    const int h = (int)((i / W) % H);
+    const long plane = i / ((long)W * H);
+    const int c = (int)(plane % C);
+    const T *g = dy + plane * P * Q;
+    float acc = 0.f;
+    for (int k = 0; k < K; ++k) {
+        const int a = h - oh[c * K + k], b = v - ow[c * K + k];
+        if (a < 0 || b < 0 || a % str || b % str) continue;
+        const int p = a / str, q = b / str;
+        if (p >= P || q >= Q) continue;
+        acc = fmaf(ld_act<T>(g + p * Q + q), w[c * K + k], acc);
+    }
+    dx[i] = to_act<T>(acc);
+}
+
+struct BwdWArgs {
+    const void *x, *dy;
+    float *ws;
+    const int16_t *oh, *ow;
+    int C, H, W, P, Q, str, K;
+    int minOH, maxOH, minOW;
+    int band, bands;
+    int tileRows, tileCols, pitch;
+};
+
+// Reduce 32 per-lane values so that lane L ends with sum over lanes of v[L] (31 shuffles).
+__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = lane & s;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const float send = upper ? v[i] : v[i + s];
+            const float keep = upper ? v[i + s] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return v[0];
+}
+
+// ws[plane*bands + band][k] = sum over the band's outputs of dy[p][q] * x[str*p+oh_k][str*q+ow_k]
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a) {
+    extern __shared__ float sm[];
+    __shared__ float red[kThreads / 32][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int plane = blockIdx.x / a.bands;
+    const int bnd = blockIdx.x - plane * a.bands;
+    const int c = plane % a.C;
+    const int p0 = bnd * a.band;
+    const int nrows = min(a.band, a.P - p0);
+    float *tile = sm;
+    float *sdy = tile + a.tileRows * a.pitch;
+    int *toff = reinterpret_cast<int *>(sdy + a.band * a.Q);
+    for (int k = tid; k < a.K; k += blockDim.x)
+        toff[k] = (a.oh[c * a.K + k] - a.minOH) * a.pitch + (a.ow[c * a.K + k] - a.minOW);
+    const T *x = static_cast<const T *>(a.x) + (size_t)plane * a.H * a.W;
+    const T *dy = static_cast<const T *>(a.dy) + (size_t)plane * a.P * a.Q + (size_t)p0 * a.Q;
+    const int h0 = a.str * p0 + a.minOH;
+    const int rows = a.str * (nrows - 1) + 1 + (a.maxOH - a.minOH);
+    for (int i = tid; i < rows * a.tileCols; i += blockDim.x) {
+        const int r = i / a.tileCols, j = i - r * a.tileCols;
+        const int h = h0 + r, v = a.minOW + j;
+        tile[r * a.pitch + j] = (h >= 0 && h < a.H && v >= 0 && v < a.W) ? ld_act<T>(x + (size_t)h * a.W + v) : 0.f;
+    }
+    for (int i = tid; i < nrows * a.Q; i += blockDim.x) sdy[i] = ld_act<T>(dy + i);
+    __syncthreads();
+    float *ws = a.ws + (size_t)blockIdx.x * a.K;
+    for (int k0 = 0; k0 < a.K; k0 += 32) {
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        const int kn = min(32, a.K - k0);
+        for (int g = tid; g < nrows * a.Q; g += blockDim.x) {
+            const int pr = g / a.Q, q = g - pr * a.Q;
+            const float gv = sdy[g];
+            const float *base = tile + pr * a.str * a.pitch + q * a.str;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < kn) acc[j] = fmaf(gv, base[toff[k0 + j]], acc[j]);
+        }
+        const float r = warp_reduce_scatter32(acc);
+        red[warp][lane] = r;
+        __syncthreads();
+        if (tid < 32 && tid < kn) {
+            float s = 0.f;
+            for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) s += red[wi][tid];
+            ws[k0 + tid] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// dW[c][k] = sum_n sum_band ws[(n*C + c)*bands + band][k], f64 accumulation, fixed order
+__global__ void bwd_weight_finalize_kernel(const float *ws, float *dW, int N, int C, int K, int bands) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C * K) return;
+    const int c = i / K, k = i - c * K;
+    double s = 0.0;
+    for (int n = 0; n < N; ++n)
+        for (int b = 0; b < bands; ++b) s += (double)ws[((size_t)(n * C + c) * bands + b) * K + k];
+    dW[i] = (float)s;
+}
+
+o1d_status check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(O1D_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    return O1D_OK;
+}
+
+template <typename F>
+o1d_status dispatch_dtype(int dt, F &&f) {
+    switch (dt) {
+        case O1D_F32: return f(float());
+        case O1D_BF16: return f(__nv_bfloat16());
+        case O1D_F16: return f(__half());
+    }
+    return fail(O1D_UNSUPPORTED, "dtype");
+}
+
+void tile_geometry(const Stencil &st, int band, int *rows, int *cols, int *pitch) {
+    *rows = st.str * (band - 1) + 1 + (st.maxDH - st.minDH);
+    *cols = st.str * (st.Wo - 1) + 1 + (st.maxDW - st.minDW);
+    int p = *cols;
+    if ((p & 31) == 0) p += 1;  // avoid a power-of-two pitch
+    *pitch = p;
+}
+
+size_t stencil_smem(const Stencil &st, int band, int extra_rows_per_out) {
+    int rows, cols, pitch;
+    tile_geometry(st, band, &rows, &cols, &pitch);
+    return sizeof(float) * ((size_t)rows * pitch + 8 * st.str + pitch + 2 * st.K +
+                            (size_t)extra_rows_per_out * band * st.Wo);
+}
+
+}  // namespace
+
+size_t dtype_size(int dt) { return dt == O1D_F32 ? 4 : 2; }
+
+int generic_band_rows(const o1d_plan *, const Stencil &st, int extra) {
+    int band = st.Ho;
+    while (band > 1 && stencil_smem(st, band, extra) > (size_t)kSmemBudget) band = (band + 1) / 2;
+    if (stencil_smem(st, band, extra) > (size_t)kSmemBudget) return 0;
+    return band;
+}
+
+o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, const void *in, const float *w,
+                           void *out, void *stream) {
+    StencilArgs a;
+    a.in = in; a.w = w; a.out = out; a.dh = st.d_dh; a.dw = st.d_dw;
+    a.C = pl->d.C; a.Hi = st.Hi; a.Wi = st.Wi; a.Ho = st.Ho; a.Wo = st.Wo; a.str = st.str; a.K = st.K;
+    a.minDH = st.minDH; a.maxDH = st.maxDH; a.minDW = st.minDW;
+    a.band = band; a.bands = (st.Ho + band - 1) / band;
+    tile_geometry(st, band, &a.tileRows, &a.tileCols, &a.pitch);
+    const size_t smem = stencil_smem(st, band, 0);
+    const long grid = (long)pl->d.N * pl->d.C * a.bands;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return dispatch_dtype(pl->d.dtype, [&](auto tag) -> o1d_status {
+        using T = decltype(tag);
+        auto kern = stencil_generic_kernel<T>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return check_launch("stencil_generic attr");
+        kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
+        return check_launch("stencil_generic");
+    });
+}
+
+o1d_status generic_bwd_input_strided(const o1d_plan *pl, const void *dy, const float *w, void *dx, void *stream) {
+    const o1d_desc &d = pl->d;
+    const long total = (long)d.N * d.C * d.H * d.W;
+    const unsigned grid = (unsigned)((total + kThreads - 1) / kThreads);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
+        using T = decltype(tag);
+        bwd_input_strided_kernel<T><<<grid, kThreads, 0, s>>>(static_cast<const T *>(dy), w, static_cast<T *>(dx),
+                                                              pl->d_oh, pl->d_ow, d.C, d.H, d.W, pl->P, pl->Q,
+                                                              d.K, d.stride, total);
+        return check_launch("bwd_input_strided");
+    });
+}
+
+o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy, float *dW, float *ws,
+                              void *stream) {
+    const o1d_desc &d = pl->d;
+    const Stencil &st = pl->fwd;
+    BwdWArgs a;
+    a.x = x; a.dy = dy; a.ws = ws; a.oh = pl->d_oh; a.ow = pl->d_ow;
+    a.C = d.C; a.H = d.H; a.W = d.W; a.P = pl->P; a.Q = pl->Q; a.str = d.stride; a.K = d.K;
+    a.minOH = st.minDH; a.maxOH = st.maxDH; a.minOW = st.minDW;
+    a.band = pl->bw_band; a.bands = pl->bw_bands;
+    tile_geometry(st, a.band, &a.tileRows, &a.tileCols, &a.pitch);
+    const size_t smem = sizeof(float) * ((size_t)a.tileRows * a.pitch + (size_t)a.band * a.Q + d.K);
+    const long grid = (long)d.N * d.C * a.bands;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    o1d_status r = dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
+        using T = decltype(tag);
+        auto kern = bwd_weight_generic_kernel<T>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return check_launch("bwd_weight_generic attr");
+        kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
+        return check_launch("bwd_weight_generic");
+    });
+    if (r != O1D_OK) return r;
+    const int n = d.C * d.K;
+    bwd_weight_finalize_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, dW, d.N, d.C, d.K, a.bands);
+    return check_launch("bwd_weight_finalize");
+}
+
+}  // namespace o1d

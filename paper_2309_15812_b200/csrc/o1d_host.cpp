@@ -1,0 +1,327 @@
+// o1d_host.cpp — host side of liboriented1d: the C ABI entry points, tap
+// generation (P:1263-1264 with reading R3), plan creation and validation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "o1d_internal.h"
+#include "o1d_spec.h"
+
+namespace o1d {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+o1d_status fail(o1d_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+// floor of the exact real value v ~= m*sin(theta) (reading R3): f64 evaluation,
+// snapped to the nearest integer when within 1e-9 of it.  The smallest true
+// distance to an integer over every angle set we support is ~4.7e-6,
+// far above both the snap radius and the f64 error (~1e-14).
+int floor_snap(double v) {
+    const double r = std::nearbyint(v);
+    if (std::fabs(v - r) < 1e-9) return (int)r;
+    return (int)std::floor(v);
+}
+
+void make_taps_one(int K, int pad, double theta_deg, int16_t *oh, int16_t *ow) {
+    double t = std::fmod(theta_deg, 360.0);  // exact
+    if (t < 0) t += 360.0;
+    const double rad = t * (M_PI / 180.0);
+    const double s = std::sin(rad), c = std::cos(rad);
+    for (int k = 0; k < K; ++k) {
+        const double m = (double)(k - pad);
+        oh[k] = (int16_t)floor_snap(-m * s);
+        ow[k] = (int16_t)floor_snap(m * c);
+    }
+}
+
+}  // namespace o1d
+
+using namespace o1d;
+
+extern "C" {
+
+const char *o1d_last_error(void) { return g_err.c_str(); }
+const char *o1d_version(void) { return "liboriented1d 0.1 (sm_100a)"; }
+
+o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles_deg, int16_t *oh, int16_t *ow) {
+    if (!angles_deg || !oh || !ow) return fail(O1D_INVALID_ARG, "o1d_make_taps: NULL pointer");
+    if (K < 1) return fail(O1D_INVALID_CONFIG, "o1d_make_taps: K < 1");
+    if (C < 1) return fail(O1D_INVALID_SHAPE, "o1d_make_taps: C < 1");
+    if (pad < 0) pad = K / 2;
+    if (pad >= K) return fail(O1D_INVALID_CONFIG, "o1d_make_taps: pad >= K");
+    for (int c = 0; c < C; ++c) {
+        if (!std::isfinite(angles_deg[c])) return fail(O1D_INVALID_ARG, "o1d_make_taps: non-finite angle");
+        make_taps_one(K, pad, angles_deg[c], oh + (size_t)c * K, ow + (size_t)c * K);
+    }
+    return O1D_OK;
+}
+
+o1d_status o1d_direction_angles(int32_t D, int32_t C, int32_t assign, double shift_deg, double *out) {
+    if (!out) return fail(O1D_INVALID_ARG, "o1d_direction_angles: NULL out");
+    if (C < 1) return fail(O1D_INVALID_SHAPE, "o1d_direction_angles: C < 1");
+    if (D < 1 || (C % D != 0 && D != C)) return fail(O1D_INVALID_CONFIG, "o1d_direction_angles: D must divide C (or D == C)");
+    if (assign != O1D_ASSIGN_CONTIGUOUS && assign != O1D_ASSIGN_CYCLED)
+        return fail(O1D_INVALID_ARG, "o1d_direction_angles: bad assign");
+    for (int c = 0; c < C; ++c) {
+        const long g = assign == O1D_ASSIGN_CONTIGUOUS ? ((long)c * D) / C : c % D;
+        // i*180/D is exact in f64 whenever D's odd part divides 180*i exactly or is a power of 2 times it
+        double a = (180.0 * (double)g) / (double)D;
+        if (shift_deg != 0.0) {
+            a = std::fmod(a + shift_deg, 180.0);
+            if (a < 0) a += 180.0;
+        }
+        out[c] = a;
+    }
+    return O1D_OK;
+}
+
+static o1d_status validate_desc(const o1d_desc *d) {
+    if (!d) return fail(O1D_INVALID_ARG, "NULL descriptor");
+    if (d->N < 1 || d->C < 1 || d->H < 1 || d->W < 1) return fail(O1D_INVALID_SHAPE, "N, C, H, W must be >= 1");
+    if (d->K < 1) return fail(O1D_INVALID_CONFIG, "K must be >= 1");
+    if (d->stride < 1) return fail(O1D_INVALID_CONFIG, "stride must be >= 1");
+    if (d->pad >= d->K) return fail(O1D_INVALID_CONFIG, "pad must be < K");
+    if (d->pad < -1) return fail(O1D_INVALID_CONFIG, "pad must be >= 0 (or -1 for floor(K/2))");
+    if (d->dtype != O1D_F32 && d->dtype != O1D_BF16 && d->dtype != O1D_F16)
+        return fail(O1D_UNSUPPORTED, "dtype must be O1D_F32, O1D_BF16 or O1D_F16");
+    if (d->layout != O1D_NCHW) return fail(O1D_UNSUPPORTED, "only the NCHW-contiguous layout is implemented");
+    if ((long)d->N * d->C * d->H * d->W > (1L << 40)) return fail(O1D_UNSUPPORTED, "tensor too large");
+    if (d->K > 1023) return fail(O1D_UNSUPPORTED, "K > 1023");
+    return O1D_OK;
+}
+
+o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan **out) {
+    if (!out) return fail(O1D_INVALID_ARG, "o1d_plan_create: NULL out");
+    *out = nullptr;
+    if (o1d_status st = validate_desc(d)) return st;
+    if (!angles_deg) return fail(O1D_INVALID_ARG, "o1d_plan_create: NULL angles");
+    o1d_plan *pl = new (std::nothrow) o1d_plan();
+    if (!pl) return fail(O1D_INVALID_ARG, "out of host memory");
+    pl->d = *d;
+    pl->pad = d->pad < 0 ? d->K / 2 : d->pad;
+    pl->d.pad = pl->pad;
+    pl->P = (d->H - 1) / d->stride + 1;
+    pl->Q = (d->W - 1) / d->stride + 1;
+    const int C = d->C, K = d->K;
+    pl->angles.assign(angles_deg, angles_deg + C);
+    pl->oh.resize((size_t)C * K);
+    pl->ow.resize((size_t)C * K);
+    if (o1d_status st = o1d_make_taps(K, pl->pad, C, angles_deg, pl->oh.data(), pl->ow.data())) {
+        delete pl;
+        return st;
+    }
+    // distinct tables, halo extents
+    std::map<std::vector<int16_t>, int> ids;
+    pl->table_of.resize(C);
+    pl->minOH = pl->minOW = 1 << 20;
+    pl->maxOH = pl->maxOW = -(1 << 20);
+    for (int c = 0; c < C; ++c) {
+        std::vector<int16_t> key(2 * K);
+        for (int k = 0; k < K; ++k) {
+            key[2 * k] = pl->oh[c * K + k];
+            key[2 * k + 1] = pl->ow[c * K + k];
+            pl->minOH = std::min<int>(pl->minOH, pl->oh[c * K + k]);
+            pl->maxOH = std::max<int>(pl->maxOH, pl->oh[c * K + k]);
+            pl->minOW = std::min<int>(pl->minOW, pl->ow[c * K + k]);
+            pl->maxOW = std::max<int>(pl->maxOW, pl->ow[c * K + k]);
+        }
+        auto it = ids.find(key);
+        if (it == ids.end()) it = ids.emplace(key, (int)ids.size()).first;
+        pl->table_of[c] = it->second;
+    }
+    pl->n_distinct = (int)ids.size();
+    // device tables: oh, ow, -oh, -ow
+    if (cudaGetDevice(&pl->device) != cudaSuccess) {
+        delete pl;
+        return fail(O1D_CUDA_ERROR, std::string("cudaGetDevice: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    const size_t tb = sizeof(int16_t) * (size_t)C * K;
+    std::vector<int16_t> host(4 * (size_t)C * K);
+    for (size_t i = 0; i < (size_t)C * K; ++i) {
+        host[i] = pl->oh[i];
+        host[(size_t)C * K + i] = pl->ow[i];
+        host[2 * (size_t)C * K + i] = (int16_t)-pl->oh[i];
+        host[3 * (size_t)C * K + i] = (int16_t)-pl->ow[i];
+    }
+    if (cudaMalloc(&pl->d_block, 4 * tb) != cudaSuccess ||
+        cudaMemcpy(pl->d_block, host.data(), 4 * tb, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaError_t e = cudaGetLastError();
+        if (pl->d_block) cudaFree(pl->d_block);
+        delete pl;
+        return fail(O1D_CUDA_ERROR, std::string("plan tables: ") + cudaGetErrorString(e));
+    }
+    int16_t *base = static_cast<int16_t *>(pl->d_block);
+    pl->d_oh = base;
+    pl->d_ow = base + (size_t)C * K;
+    pl->d_noh = base + 2 * (size_t)C * K;
+    pl->d_now = base + 3 * (size_t)C * K;
+    // stencil geometry of the forward and (stride 1) backward_input passes
+    pl->fwd = Stencil{d->H, d->W, pl->P, pl->Q, d->stride, K, pl->minOH, pl->maxOH, pl->minOW, pl->maxOW,
+                      pl->d_oh, pl->d_ow};
+    pl->bwd_in = Stencil{pl->P, pl->Q, d->H, d->W, 1, K, -pl->maxOH, -pl->minOH, -pl->maxOW, -pl->minOW,
+                         pl->d_noh, pl->d_now};
+    pl->fwd_band = generic_band_rows(pl, pl->fwd, 0);
+    pl->bi_band = d->stride == 1 ? generic_band_rows(pl, pl->bwd_in, 0) : 1;
+    pl->bw_band = generic_band_rows(pl, pl->fwd, 1);
+    if (pl->fwd_band == 0 || pl->bi_band == 0 || pl->bw_band == 0) {
+        o1d_plan_destroy(pl);
+        return fail(O1D_UNSUPPORTED, "image row (plus halo) does not fit in shared memory");
+    }
+    pl->bw_bands = (pl->P + pl->bw_band - 1) / pl->bw_band;
+    pl->ws_bytes = sizeof(float) * (size_t)d->N * C * pl->bw_bands * K;
+    char buf[256];
+    snprintf(buf, sizeof buf, "generic(fwd band %d, bwd_in band %d, bwd_w band %d), %d distinct tap tables",
+             pl->fwd_band, pl->bi_band, pl->bw_band, pl->n_distinct);
+    pl->describe = buf;
+    if (!(d->flags & O1D_FLAG_FORCE_GENERIC)) {
+        o1d_status st = spec_create(pl);
+        if (st != O1D_OK) {
+            o1d_plan_destroy(pl);
+            return st;
+        }
+    }
+    *out = pl;
+    return O1D_OK;
+}
+
+void o1d_plan_destroy(o1d_plan *pl) {
+    if (!pl) return;
+    spec_destroy(pl);
+    if (pl->d_block) cudaFree(pl->d_block);
+    delete pl;
+}
+
+o1d_status o1d_plan_out_shape(const o1d_plan *pl, int32_t *P, int32_t *Q) {
+    if (!pl || !P || !Q) return fail(O1D_INVALID_ARG, "o1d_plan_out_shape: NULL pointer");
+    *P = pl->P;
+    *Q = pl->Q;
+    return O1D_OK;
+}
+
+o1d_status o1d_plan_get_taps(const o1d_plan *pl, int16_t *oh, int16_t *ow) {
+    if (!pl || !oh || !ow) return fail(O1D_INVALID_ARG, "o1d_plan_get_taps: NULL pointer");
+    std::memcpy(oh, pl->oh.data(), pl->oh.size() * sizeof(int16_t));
+    std::memcpy(ow, pl->ow.data(), pl->ow.size() * sizeof(int16_t));
+    return O1D_OK;
+}
+
+const char *o1d_plan_describe(const o1d_plan *pl) { return pl ? pl->describe.c_str() : ""; }
+
+size_t o1d_workspace_bytes(const o1d_plan *pl) {
+    if (!pl) return 0;
+    return std::max(pl->ws_bytes, spec_workspace_bytes(pl));
+}
+
+static o1d_status check_ptr(const void *p, const char *name) {
+    if (!p) return fail(O1D_INVALID_ARG, std::string(name) + " is NULL");
+    if (reinterpret_cast<uintptr_t>(p) & 15) return fail(O1D_MISALIGNED, std::string(name) + " is not 16-byte aligned");
+    return O1D_OK;
+}
+
+static o1d_status check_device(const o1d_plan *pl) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(O1D_CUDA_ERROR, "cudaGetDevice failed");
+    if (dev != pl->device) return fail(O1D_INVALID_ARG, "current device differs from the plan's device");
+    return O1D_OK;
+}
+
+o1d_status o1d_forward(const o1d_plan *pl, const void *x, const float *w, void *y, void *stream) {
+    if (!pl) return fail(O1D_INVALID_ARG, "NULL plan");
+    if (o1d_status st = check_ptr(x, "x")) return st;
+    if (o1d_status st = check_ptr(w, "w")) return st;
+    if (o1d_status st = check_ptr(y, "y")) return st;
+    if (o1d_status st = check_device(pl)) return st;
+    if (pl->spec && spec_has(pl, 0)) return spec_run(pl, 0, x, w, y, nullptr, nullptr, stream);
+    return generic_stencil(pl, pl->fwd, pl->fwd_band, x, w, y, stream);
+}
+
+o1d_status o1d_backward_input(const o1d_plan *pl, const void *dy, const float *w, void *dx, void *stream) {
+    if (!pl) return fail(O1D_INVALID_ARG, "NULL plan");
+    if (o1d_status st = check_ptr(dy, "dy")) return st;
+    if (o1d_status st = check_ptr(w, "w")) return st;
+    if (o1d_status st = check_ptr(dx, "dx")) return st;
+    if (o1d_status st = check_device(pl)) return st;
+    if (pl->spec && spec_has(pl, 1)) return spec_run(pl, 1, dy, w, dx, nullptr, nullptr, stream);
+    if (pl->d.stride == 1) return generic_stencil(pl, pl->bwd_in, pl->bi_band, dy, w, dx, stream);
+    return generic_bwd_input_strided(pl, dy, w, dx, stream);
+}
+
+o1d_status o1d_backward_weight(const o1d_plan *pl, const void *x, const void *dy, float *dW, void *ws,
+                               size_t ws_bytes, void *stream) {
+    if (!pl) return fail(O1D_INVALID_ARG, "NULL plan");
+    if (o1d_status st = check_ptr(x, "x")) return st;
+    if (o1d_status st = check_ptr(dy, "dy")) return st;
+    if (o1d_status st = check_ptr(dW, "dW")) return st;
+    if (o1d_status st = check_ptr(ws, "ws")) return st;
+    if (ws_bytes < o1d_workspace_bytes(pl))
+        return fail(O1D_WORKSPACE_TOO_SMALL, "ws_bytes < o1d_workspace_bytes(plan)");
+    if (o1d_status st = check_device(pl)) return st;
+    if (pl->spec && spec_has(pl, 2)) return spec_run(pl, 2, x, nullptr, dy, dW, static_cast<float *>(ws), stream);
+    return generic_bwd_weight(pl, x, dy, dW, static_cast<float *>(ws), stream);
+}
+
+int32_t o1d_launches_per_call(const o1d_plan *pl, int32_t pass) {
+    if (!pl) return 0;
+    if (pl->spec && spec_has(pl, pass)) return spec_launches(pl, pass);
+    return pass == 2 ? 2 : 1;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+size_t o1d_step_host_workspace_bytes(const o1d_plan *pl) {
+    if (!pl) return 0;
+    const size_t es = dtype_size(pl->d.dtype);
+    const size_t nx = (size_t)pl->d.N * pl->d.C * pl->d.H * pl->d.W * es;
+    const size_t ny = (size_t)pl->d.N * pl->d.C * pl->P * pl->Q * es;
+    const size_t nw = sizeof(float) * (size_t)pl->d.C * pl->d.K;
+    return 2 * align256(nx) + 2 * align256(ny) + 2 * align256(nw) + align256(o1d_workspace_bytes(pl));
+}
+
+o1d_status o1d_step_host(const o1d_plan *pl, const void *x_h, const float *w_h, const void *dy_h, void *y_h,
+                         void *dx_h, float *dW_h, void *dev_ws, size_t dev_ws_bytes, void *stream) {
+    if (!pl || !x_h || !w_h || !dy_h || !y_h || !dx_h || !dW_h) return fail(O1D_INVALID_ARG, "o1d_step_host: NULL pointer");
+    if (o1d_status st = check_ptr(dev_ws, "dev_ws")) return st;
+    if (dev_ws_bytes < o1d_step_host_workspace_bytes(pl))
+        return fail(O1D_WORKSPACE_TOO_SMALL, "dev_ws_bytes < o1d_step_host_workspace_bytes(plan)");
+    const size_t es = dtype_size(pl->d.dtype);
+    const size_t nx = (size_t)pl->d.N * pl->d.C * pl->d.H * pl->d.W * es;
+    const size_t ny = (size_t)pl->d.N * pl->d.C * pl->P * pl->Q * es;
+    const size_t nw = sizeof(float) * (size_t)pl->d.C * pl->d.K;
+    char *b = static_cast<char *>(dev_ws);
+    void *x = b; b += align256(nx);
+    void *dx = b; b += align256(nx);
+    void *y = b; b += align256(ny);
+    void *dy = b; b += align256(ny);
+    float *w = reinterpret_cast<float *>(b); b += align256(nw);
+    float *dW = reinterpret_cast<float *>(b); b += align256(nw);
+    void *ws = b;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(x, x_h, nx, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(w, w_h, nw, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(dy, dy_h, ny, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return fail(O1D_CUDA_ERROR, std::string("H2D: ") + cudaGetErrorString(cudaGetLastError()));
+    if (o1d_status st = o1d_forward(pl, x, w, y, stream)) return st;
+    if (o1d_status st = o1d_backward_input(pl, dy, w, dx, stream)) return st;
+    if (o1d_status st = o1d_backward_weight(pl, x, dy, dW, ws, o1d_workspace_bytes(pl), stream)) return st;
+    if (cudaMemcpyAsync(y_h, y, ny, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(dx_h, dx, nx, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(dW_h, dW, nw, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return fail(O1D_CUDA_ERROR, std::string("D2H: ") + cudaGetErrorString(cudaGetLastError()));
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(O1D_CUDA_ERROR, std::string("o1d_step_host: ") + cudaGetErrorString(cudaGetLastError()));
+    return O1D_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the header
+declares, and its host functions (tap tables, angle assignment, validation) agree
+with the oracle.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import taps as T
+from paper_2309_15812_b200 import binding as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2309_15812_b200 import build
+    build.build()
+    B.lib()
+
+
+def test_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "oriented1d.h")).read()
+    declared = set(re.findall(r"O1D_API[^;(]*?\b(o1d_\w+)\s*\(", hdr))
+    assert len(declared) >= 16
+    L = ctypes.CDLL(B.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(B.EXPORTS) == declared
+    assert "sm_100a" in B.version()
+
+
+def _angle_sets():
+    sets = {}
+    for D in (2, 4, 8):
+        for assign in ("contiguous", "cycled"):
+            sets[f"D{D}_{assign}"] = T.direction_angles(D, 8 * D, assign)
+    for C in (8, 96, 128, 192, 256, 384, 512, 768, 1024):
+        sets[f"D=C={C}"] = T.direction_angles(C, C)
+    sets["integer_deg"] = [float(a) for a in range(360)]
+    sets["half_deg"] = [a * 0.5 for a in range(720)]
+    sets["negative"] = [-a * 7.5 for a in range(48)]
+    return sets
+
+
+@pytest.mark.parametrize("K", [3, 5, 7, 15, 27, 31, 63])
+def test_make_taps_bit_exact_vs_oracle(K):
+    """T1: the library's f64+snap tap generator equals the exact-math oracle bit for bit."""
+    for name, angles in _angle_sets().items():
+        oh, ow = B.make_taps(K, np.array(angles))
+        roh, row = T.taps_table(K, K // 2, angles)
+        assert np.array_equal(oh, np.array(roh, np.int16)), (name, K)
+        assert np.array_equal(ow, np.array(row, np.int16)), (name, K)
+
+
+def test_make_taps_nondefault_pad():
+    angles = np.array([0.0, 22.5, 45.0, 90.0, 135.0, 300.0])
+    for K, pad in ((7, 0), (7, 6), (8, 4), (6, 2)):
+        oh, ow = B.make_taps(K, angles, pad=pad)
+        roh, row = T.taps_table(K, pad, angles)
+        assert np.array_equal(oh, np.array(roh)) and np.array_equal(ow, np.array(row))
+
+
+def test_direction_angles_vs_oracle():
+    for D, C in ((4, 8), (8, 96), (8, 384), (96, 96), (768, 768), (2, 4)):
+        for assign in ("contiguous", "cycled"):
+            for shift in (0.0, 90.0):
+                got = B.direction_angles(D, C, assign, shift)
+                assert got.tolist() == T.direction_angles(D, C, assign, shift), (D, C, assign, shift)
+
+
+def test_error_codes():
+    with pytest.raises(B.O1DError) as e:
+        B.direction_angles(3, 8)
+    assert e.value.status == 3 and "divide" in str(e.value)
+    with pytest.raises(B.O1DError) as e:
+        B.make_taps(0, np.zeros(2))
+    assert e.value.status == 3
+    L = B.lib()
+    h = ctypes.c_void_p()
+    ang = np.zeros(4)
+    for fields, status in (((0, 4, 8, 8, 3, 1, -1, 0, 0, 0), 2),  # N = 0
+                           ((1, 4, 8, 8, 0, 1, -1, 0, 0, 0), 3),  # K = 0
+                           ((1, 4, 8, 8, 3, 0, -1, 0, 0, 0), 3),  # stride 0
+                           ((1, 4, 8, 8, 3, 1, 3, 0, 0, 0), 3),   # pad >= K
+                           ((1, 4, 8, 8, 3, 1, -1, 7, 0, 0), 5),  # dtype
+                           ((1, 4, 8, 8, 3, 1, -1, 0, 1, 0), 5)):  # layout
+        d = B._Desc(*fields)
+        st = L.o1d_plan_create(ctypes.byref(d), B._ptr(ang), ctypes.byref(h))
+        assert st == status, (fields, st, L.o1d_last_error())
+        assert not h.value
+    assert L.o1d_forward(None, None, None, None, None) == 1

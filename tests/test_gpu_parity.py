@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on identical
+seeded inputs.  Tolerances (BASELINE.json north_star, reading R9): normwise
+max|g - r| / max|r| <= 1e-5 for fp32, <= 2e-2 for bf16/fp16 (fp32 accumulation);
+tap tables bit-exact; results bitwise deterministic."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import taps as T
+from paper_2309_15812_b200 import binding as B
+from paper_2309_15812_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2, torch.float16: 2e-2}
+NP_DT = {torch.float32: "f32", torch.bfloat16: "bf16", torch.float16: "f16"}
+
+
+def nerr(g: torch.Tensor, r: np.ndarray) -> float:
+    g = g.double().cpu().numpy()
+    den = float(np.max(np.abs(r)))
+    return float(np.max(np.abs(g - r))) / (den if den > 0 else 1.0)
+
+
+_oracle_cache = {}
+
+
+def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, threads=None, check_det=False):
+    angles = [float(a) for a in angles]
+    plan = B.Plan(N, C, H, W, K, np.array(angles), stride=stride, dtype=dtype, flags=flags, device="cuda:0")
+    P, Q = plan.P, plan.Q
+    dt = NP_DT[dtype]
+    x = inputs.activation((N, C, H, W), 0, dt)
+    w = inputs.weights(C, K, 1)
+    dy = inputs.activation((N, C, P, Q), 2, dt)
+    key = (N, C, H, W, K, tuple(angles), stride, dt)
+    if key not in _oracle_cache:
+        oh, ow = T.taps_table(K, K // 2, angles)
+        oh, ow = np.array(oh, np.int32), np.array(ow, np.int32)
+        th = threads or max(1, oracle.max_threads())
+        _oracle_cache.clear()
+        _oracle_cache[key] = (oh, ow, oracle.forward(x, w, oh, ow, stride, th),
+                              oracle.backward_input(dy, w, oh, ow, H, W, stride, th),
+                              oracle.backward_weight(x, dy, oh, ow, stride, th))
+    oh, ow, ry, rdx, rdW = _oracle_cache[key]
+    poh, pow_ = plan.taps()
+    assert np.array_equal(poh, oh) and np.array_equal(pow_, ow), "tap tables must be bit-exact"
+    tx = torch.from_numpy(x).to("cuda:0", dtype)
+    tdy = torch.from_numpy(dy).to("cuda:0", dtype)
+    tw = torch.from_numpy(w).cuda()
+    y = B.forward(plan, tx, tw)
+    dx = B.backward_input(plan, tdy, tw)
+    dW = B.backward_weight(plan, tx, tdy)
+    torch.cuda.synchronize()
+    errs = {"y": nerr(y, ry), "dx": nerr(dx, rdx), "dW": nerr(dW, rdW)}
+    tol = TOL[dtype]
+    assert all(e <= tol for e in errs.values()), (plan.describe(), errs)
+    if check_det:
+        y2 = B.forward(plan, tx, tw)
+        dx2 = B.backward_input(plan, tdy, tw)
+        dW2 = B.backward_weight(plan, tx, tdy)
+        assert torch.equal(y, y2) and torch.equal(dx, dx2) and torch.equal(dW, dW2)
+    return plan, errs
+
+
+FLAGS = {"default": 0, "generic": B.FLAG_FORCE_GENERIC}
+
+
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("assign", ["cycled", "contiguous"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_tiny(flags, assign, dtype, stride):
+    # BASELINE configs[0]: N=1, C=8, 14x14, K=7, {0,45,90,135} deg
+    angles = T.direction_angles(4, 8, assign)
+    run_case(1, 8, 14, 14, 7, angles, stride, dtype, FLAGS[flags], check_det=True)
+
+
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("HW", [(56, 56), (37, 45), (61, 29), (7, 9), (1, 1), (1, 40), (40, 1)])
+def test_stage1_like_ragged(flags, dtype, HW):
+    """K=31, 8 angles, multiple tiles with ragged edges, degenerate 1-pixel images."""
+    H, W = HW
+    run_case(2, 16, H, W, 31, T.direction_angles(8, 16, "cycled"), 1, dtype, FLAGS[flags], check_det=True)
+
+
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("K", [1, 3, 7, 15, 23, 31, 39, 47, 55, 63])
+def test_ksweep_shape(flags, K):
+    # configs[2] geometry (14x14, D=8 cycled) at a reduced N, C
+    run_case(2, 16, 14, 14, K, T.direction_angles(8, 16, "cycled"), 1, torch.float32, FLAGS[flags])
+
+
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("angle_set", ["thirties_DC96", "integer_deg", "single_45", "neg_and_big"])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_angle_sets(flags, angle_set, stride):
+    if angle_set == "thirties_DC96":
+        angles, C = T.direction_angles(96, 96), 96
+    elif angle_set == "integer_deg":
+        angles, C = [float((37 * c) % 360) for c in range(24)], 24
+    elif angle_set == "single_45":
+        angles, C = [45.0] * 8, 8
+    else:
+        angles, C = [-30.0, 725.5, -3600.0, 1e3, 89.999, 90.001, 180.0, 270.0], 8
+    run_case(1, C, 30, 23, 15, angles, stride, torch.float32, FLAGS[flags])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_full_stage1_config(dtype):
+    """BASELINE configs[1] at full size, in the launch configuration bench.py times."""
+    wl = inputs.S1
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan, errs = run_case(wl.N, wl.C, wl.H, wl.W, wl.K, angles, 1, dtype, 0)
+    print(plan.describe(), errs)
+
+
+def test_errors_on_gpu():
+    plan = B.Plan(1, 8, 14, 14, 7, np.zeros(8), device="cuda:0")
+    x = torch.zeros(1, 8, 14, 14, device="cuda:0")
+    w = torch.zeros(8, 7, device="cuda:0")
+    with pytest.raises(ValueError):
+        B.forward(plan, x.transpose(2, 3), w)  # non-contiguous is an error, never a silent copy
+    with pytest.raises(ValueError):
+        B.forward(plan, x.half(), w)
+    ws = torch.zeros(1, device="cuda:0")
+    with pytest.raises(B.O1DError) as e:
+        B.backward_weight(plan, x, x, ws=ws)
+    assert e.value.status == 7
+    import ctypes
+    L = B.lib()
+    st = L.o1d_forward(plan.handle, ctypes.c_void_p(x.data_ptr() + 4), ctypes.c_void_p(w.data_ptr()),
+                       ctypes.c_void_p(x.data_ptr()), None)
+    assert st == 6  # MISALIGNED
+
+
+def test_module_autograd():
+    from paper_2309_15812_b200.module import Oriented1dDWConv
+    torch.manual_seed(0)
+    m = Oriented1dDWConv(16, 7, D=8).cuda()
+    x = torch.randn(2, 16, 20, 20, device="cuda:0", requires_grad=True)
+    y = m(x)
+    y.square().sum().backward()
+    angles = m.angles_deg.cpu().numpy().tolist()
+    oh, ow = T.taps_table(7, 3, angles)
+    oh, ow = np.array(oh), np.array(ow)
+    xd = x.detach().double().cpu().numpy()
+    wd = m.weight.detach().double().cpu().numpy()
+    ry = oracle.forward(xd, wd, oh, ow)
+    assert nerr(y.detach(), ry) <= 1e-5
+    g = 2 * ry
+    assert nerr(x.grad, oracle.backward_input(g, wd, oh, ow, 20, 20)) <= 1e-5
+    assert nerr(m.weight.grad, oracle.backward_weight(xd, g, oh, ow)) <= 1e-5
+
+
+def test_step_host_matches_device_path():
+    wl = inputs.TINY
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, np.array(angles), device="cuda:0")
+    x = torch.from_numpy(inputs.activation(plan.x_shape(), 0)).pin_memory()
+    w = torch.from_numpy(inputs.weights(wl.C, wl.K)).pin_memory()
+    dy = torch.from_numpy(inputs.activation(plan.y_shape(), 2)).pin_memory()
+    y, dx, dW = torch.empty_like(x).pin_memory(), torch.empty_like(x).pin_memory(), torch.empty_like(w).pin_memory()
+    B.step_host(plan, x, w, dy, y, dx, dW, B.step_host_workspace(plan))
+    xd, wd, dyd = x.cuda(), w.cuda(), dy.cuda()
+    assert torch.equal(y, B.forward(plan, xd, wd).cpu())
+    assert torch.equal(dx, B.backward_input(plan, dyd, wd).cpu())
+    assert torch.equal(dW, B.backward_weight(plan, xd, dyd).cpu())
