@@ -87,9 +87,11 @@ typedef struct o1d_plan o1d_plan;
 
 /* Tap-offset table (Eq. coordinate, Eq. coordinate1d):
  *   oh[c*K+k] = floor(-(k-pad) * sin(angles_deg[c])),  ow[c*K+k] = floor((k-pad) * cos(angles_deg[c]))
- * evaluated as the floor of the exact real value (reading R3: f64 trig of the
- * angle reduced mod 360 deg, snapped to the nearest integer when within 1e-9 of
- * it).  angles_deg: host [C] (degrees, any real).  oh, ow: host [C][K] outputs.
+ * evaluated as the floor of the exact real value (reading R3): the angle is
+ * reduced mod 360 deg exactly; at the Niven angles (sin or cos in {0,+-1/2,+-1})
+ * the product is evaluated exactly, elsewhere it is irrational and its floor is
+ * taken from f64 trig, re-evaluated in binary128 when within 1e-9 of an integer.
+ * angles_deg: host [C] (degrees, any finite real).  oh, ow: host [C][K] outputs.
  * pad: -1 => floor(K/2).  Pure host function, no CUDA context needed. */
 O1D_API o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles_deg,
                          int16_t *oh, int16_t *ow);

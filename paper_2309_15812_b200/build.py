@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out.decode())
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs +
-                          ["-cudart", "static", "-ldl", "-lpthread", "-lrt"])
+                          ["-cudart", "static", "-lquadmath", "-ldl", "-lpthread", "-lrt"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,6 +1,7 @@
 // o1d_host.cpp — host side of liboriented1d: the C ABI entry points, tap
 // generation (P:1263-1264 with reading R3), plan creation and validation.
 #include <cuda_runtime.h>
+#include <quadmath.h>
 
 #include <algorithm>
 #include <cmath>
@@ -24,25 +25,53 @@ o1d_status fail(o1d_status st, const std::string &msg) {
     return st;
 }
 
-// floor of the exact real value v ~= m*sin(theta) (reading R3): f64 evaluation,
-// snapped to the nearest integer when within 1e-9 of it.  The smallest true
-// distance to an integer over every angle set we support is ~4.7e-6,
-// far above both the snap radius and the f64 error (~1e-14).
-int floor_snap(double v) {
-    const double r = std::nearbyint(v);
-    if (std::fabs(v - r) < 1e-9) return (int)r;
-    return (int)std::floor(v);
+// Tap rule of P:1263-1264 evaluated as the floor of the EXACT real value
+// (reading R3).  The angle is a binary double, i.e. a rational number of
+// degrees t, so by Niven's theorem sin(t) is rational only at t = 0, 30, 90,
+// 150, 180, 210, 270, 330 (mod 360) and cos(t) only at t = 0, 60, 90, 120, 180,
+// 240, 270, 300; there the product m*sin / m*cos is evaluated exactly.  Any other
+// product is irrational, never an integer: f64 gives its floor unless it lies
+// within 1e-9 of an integer, in which case it is re-evaluated in binary128
+// (__float128, 113-bit significand), exact unless the angle lies within ~1e-28
+// degrees of one of the Niven angles above.
+static bool niven_sin(double t, double *v) {  // t in [0, 360)
+    static const double a[8] = {0, 30, 90, 150, 180, 210, 270, 330};
+    static const double s[8] = {0, 0.5, 1, 0.5, 0, -0.5, -1, -0.5};
+    for (int i = 0; i < 8; ++i)
+        if (t == a[i]) { *v = s[i]; return true; }
+    return false;
 }
+static bool niven_cos(double t, double *v) {
+    static const double a[8] = {0, 60, 90, 120, 180, 240, 270, 300};
+    static const double c[8] = {1, 0.5, 0, -0.5, -1, -0.5, 0, 0.5};
+    for (int i = 0; i < 8; ++i)
+        if (t == a[i]) { *v = c[i]; return true; }
+    return false;
+}
+
+// floor(m * f(t)) for f = sin (is_sin) or cos, t in degrees reduced to [0, 360)
+static int floor_trig_times(int m, double t, bool is_sin) {
+    if (m == 0) return 0;
+    double r;
+    if (is_sin ? niven_sin(t, &r) : niven_cos(t, &r)) return (int)std::floor((double)m * r);  // exact: r in {0,+-1/2,+-1}
+    const double rad = t * (M_PI / 180.0);
+    const double v = (double)m * (is_sin ? std::sin(rad) : std::cos(rad));
+    const double n = std::nearbyint(v);
+    if (std::fabs(v - n) >= 1e-9) return (int)std::floor(v);
+    const __float128 radq = (__float128)t * (acosq((__float128)-1) / 180);
+    const __float128 vq = (__float128)m * (is_sin ? sinq(radq) : cosq(radq));
+    return (int)floorq(vq);
+}
+
 
 void make_taps_one(int K, int pad, double theta_deg, int16_t *oh, int16_t *ow) {
     double t = std::fmod(theta_deg, 360.0);  // exact
     if (t < 0) t += 360.0;
-    const double rad = t * (M_PI / 180.0);
-    const double s = std::sin(rad), c = std::cos(rad);
+    if (t >= 360.0) t -= 360.0;
     for (int k = 0; k < K; ++k) {
-        const double m = (double)(k - pad);
-        oh[k] = (int16_t)floor_snap(-m * s);
-        ow[k] = (int16_t)floor_snap(m * c);
+        const int m = k - pad;
+        oh[k] = (int16_t)floor_trig_times(-m, t, true);   // floor(-(k-pad) sin t)
+        ow[k] = (int16_t)floor_trig_times(m, t, false);   // floor( (k-pad) cos t)
     }
 }
 

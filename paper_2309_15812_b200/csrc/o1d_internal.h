@@ -15,8 +15,7 @@ namespace o1d {
 void set_error(const std::string &msg);
 o1d_status fail(o1d_status st, const std::string &msg);
 
-// Tap rule of P:1263-1264 with reading R3 (exact floor via f64 + 1e-9 snap).
-int floor_snap(double v);
+// Tap rule of P:1263-1264 with reading R3 (floor of the exact real value).
 void make_taps_one(int K, int pad, double theta_deg, int16_t *oh, int16_t *ow);
 
 // Geometry of one "stencil launch": an output plane of Ho x Wo computed from an

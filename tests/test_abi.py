@@ -42,6 +42,10 @@ def _angle_sets():
     sets["integer_deg"] = [float(a) for a in range(360)]
     sets["half_deg"] = [a * 0.5 for a in range(720)]
     sets["negative"] = [-a * 7.5 for a in range(48)]
+    eps = [1e-3, 1e-6, 1e-9, 1e-12]
+    sets["near_niven"] = [a + s * e for a in (0, 30, 60, 90, 120, 150, 180, 210, 270, 330)
+                          for e in eps for s in (-1, 1)]
+    sets["big"] = [725.5, -3600.0, 1e3, 1e6 + 0.5, -1e5 - 30.0]
     return sets
 
 
