@@ -158,6 +158,14 @@ O1D_API o1d_status o1d_step_host(const o1d_plan *plan, const void *x_h, const fl
 O1D_API int32_t o1d_launches_per_call(const o1d_plan *plan, int32_t pass /* 0 fwd, 1 bwd_in, 2 bwd_w */);
 
 O1D_API void o1d_plan_destroy(o1d_plan *plan);
+
+/* Diagnostics: the CUDA C++ source the plan's specialised kernels would be
+ * compiled from (pass 0 forward, 1 backward_input, 2 backward_weight), built on
+ * the host only (no GPU needed).  buf may be NULL to query the size; *len is
+ * in/out (buffer size in, bytes incl. the NUL out).  UNSUPPORTED when the
+ * problem is served by the generic kernels. */
+O1D_API o1d_status o1d_spec_source(const o1d_desc *d, const double *angles_deg, int32_t pass, char *buf,
+                                   size_t *len);
 O1D_API const char *o1d_last_error(void);
 O1D_API const char *o1d_version(void);
 

@@ -29,7 +29,7 @@ ASSIGN = {"contiguous": 0, "cycled": 1}
 EXPORTS = ["o1d_make_taps", "o1d_direction_angles", "o1d_plan_create", "o1d_plan_out_shape",
            "o1d_plan_get_taps", "o1d_plan_describe", "o1d_workspace_bytes", "o1d_forward",
            "o1d_backward_input", "o1d_backward_weight", "o1d_step_host_workspace_bytes", "o1d_step_host",
-           "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version"]
+           "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source"]
 
 
 class O1DError(RuntimeError):
@@ -73,6 +73,7 @@ def lib():
                 "o1d_plan_destroy": (None, [vp]),
                 "o1d_last_error": (ctypes.c_char_p, []),
                 "o1d_version": (ctypes.c_char_p, []),
+                "o1d_spec_source": (st, [ctypes.POINTER(_Desc), f64p, i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -109,6 +110,17 @@ def direction_angles(D: int, C: int, assign: str = "contiguous", shift_deg: floa
     out = np.empty(C, np.float64)
     _check(lib().o1d_direction_angles(D, C, ASSIGN[assign], float(shift_deg), _ptr(out)))
     return out
+
+
+def spec_source(N, C, H, W, K, angles_deg, pass_id: int, stride=1, pad=-1, dtype=torch.float32) -> str:
+    """CUDA source of the specialised kernel for one pass (host only, diagnostics)."""
+    a = np.ascontiguousarray(angles_deg, dtype=np.float64)
+    d = _Desc(N, C, H, W, K, stride, pad, DTYPES[dtype], 0, 0)
+    n = ctypes.c_size_t(0)
+    _check(lib().o1d_spec_source(ctypes.byref(d), _ptr(a), pass_id, None, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib().o1d_spec_source(ctypes.byref(d), _ptr(a), pass_id, buf, ctypes.byref(n)))
+    return buf.value.decode()
 
 
 def _stream_handle(stream):

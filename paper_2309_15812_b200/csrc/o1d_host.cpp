@@ -131,13 +131,10 @@ static o1d_status validate_desc(const o1d_desc *d) {
     return O1D_OK;
 }
 
-o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan **out) {
-    if (!out) return fail(O1D_INVALID_ARG, "o1d_plan_create: NULL out");
-    *out = nullptr;
+// Host-only part of plan creation: taps, distinct tables, halo extents.
+static o1d_status plan_host_init(const o1d_desc *d, const double *angles_deg, o1d_plan *pl) {
     if (o1d_status st = validate_desc(d)) return st;
     if (!angles_deg) return fail(O1D_INVALID_ARG, "o1d_plan_create: NULL angles");
-    o1d_plan *pl = new (std::nothrow) o1d_plan();
-    if (!pl) return fail(O1D_INVALID_ARG, "out of host memory");
     pl->d = *d;
     pl->pad = d->pad < 0 ? d->K / 2 : d->pad;
     pl->d.pad = pl->pad;
@@ -147,11 +144,7 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
     pl->angles.assign(angles_deg, angles_deg + C);
     pl->oh.resize((size_t)C * K);
     pl->ow.resize((size_t)C * K);
-    if (o1d_status st = o1d_make_taps(K, pl->pad, C, angles_deg, pl->oh.data(), pl->ow.data())) {
-        delete pl;
-        return st;
-    }
-    // distinct tables, halo extents
+    if (o1d_status st = o1d_make_taps(K, pl->pad, C, angles_deg, pl->oh.data(), pl->ow.data())) return st;
     std::map<std::vector<int16_t>, int> ids;
     pl->table_of.resize(C);
     pl->minOH = pl->minOW = 1 << 20;
@@ -171,6 +164,31 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
         pl->table_of[c] = it->second;
     }
     pl->n_distinct = (int)ids.size();
+    return O1D_OK;
+}
+
+o1d_status o1d_spec_source(const o1d_desc *d, const double *angles_deg, int32_t pass, char *buf, size_t *len) {
+    if (!len) return fail(O1D_INVALID_ARG, "o1d_spec_source: NULL len");
+    o1d_plan pl;
+    if (o1d_status st = plan_host_init(d, angles_deg, &pl)) return st;
+    std::string src;
+    if (o1d_status st = spec_source(&pl, pass, &src)) return st;
+    if (buf && *len > src.size()) memcpy(buf, src.c_str(), src.size() + 1);
+    *len = src.size() + 1;
+    return O1D_OK;
+}
+
+o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan **out) {
+    if (!out) return fail(O1D_INVALID_ARG, "o1d_plan_create: NULL out");
+    *out = nullptr;
+    if (o1d_status st = validate_desc(d)) return st;
+    o1d_plan *pl = new (std::nothrow) o1d_plan();
+    if (!pl) return fail(O1D_INVALID_ARG, "out of host memory");
+    if (o1d_status st = plan_host_init(d, angles_deg, pl)) {
+        delete pl;
+        return st;
+    }
+    const int C = d->C, K = d->K;
     // device tables: oh, ow, -oh, -ow
     if (cudaGetDevice(&pl->device) != cudaSuccess) {
         delete pl;

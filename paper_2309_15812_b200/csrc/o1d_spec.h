@@ -1,16 +1,20 @@
-// o1d_spec.h — runtime-specialised (JIT) kernels: one kernel per distinct tap
+// o1d_spec.h — runtime-specialised (JIT) kernels: one case per distinct tap
 // table, with the taps compiled in as constants so the register-blocked tap
 // loops get static register indexing.
 #pragma once
+#include <string>
+
 #include "o1d_internal.h"
 
 namespace o1d {
 o1d_status spec_create(o1d_plan *pl);  // may leave pl->spec == nullptr (generic only)
+// generated CUDA source of one pass (host only; diagnostics)
+o1d_status spec_source(const o1d_plan *pl, int pass, std::string *out);
 void spec_destroy(o1d_plan *pl);
 bool spec_has(const o1d_plan *pl, int pass);
 int spec_launches(const o1d_plan *pl, int pass);
 size_t spec_workspace_bytes(const o1d_plan *pl);
-// pass 0: a=x, w, out=y; pass 1: a=dy, w, out=dx; pass 2: a=x, out=dy (input), dW, ws
+// pass 0: a=x, w, b=y; pass 1: a=dy, w, b=dx; pass 2: a=x, b=dy, dW, ws
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW,
                     float *ws, void *stream);
 }  // namespace o1d
