@@ -210,13 +210,14 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 }  // namespace
 
 struct SpecSet {
-    int BR = 0, BC = 0, nthreads = 0, nwarps = 0, nt = 0;
-    int sdy_pitch = 0;
+    int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, PPC = 1, nt = 0, nsm = 0;
     std::vector<Geo> fwd, bwd;  // per distinct table
+    std::vector<int> count;     // planes per table
     CUmodule mod[3] = {nullptr, nullptr, nullptr};
     CUfunction fn[3] = {nullptr, nullptr, nullptr};
     size_t smem[3] = {0, 0, 0};
-    unsigned *d_counters = nullptr;
+    int grid[3] = {0, 0, 0};
+    unsigned *d_sched = nullptr;  // 3 passes x (NT next counters + 1 done counter), then C channel counters
     std::string regs[3];
 };
 
@@ -229,17 +230,19 @@ typedef unsigned int u32;
 struct __align__(64) TmaDesc { u64 v[16]; };
 struct Params {
   TmaDesc in_map[NT];
-  TmaDesc aux_map;
+  TmaDesc out_map;   // y / dx dense box (stencil TMA store)
   const float* w;
+  void* io;          // y (forward) / dx (backward_input) / dy (wgrad)
   float* ws;
-  unsigned* cnt;
+  unsigned* sched;   // [NT] next-plane counters, [NT] = done counter
+  unsigned* cnt;     // [C] per-channel epoch counters (wgrad)
   float* dW;
 };
 __device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect(u64* b, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sa(b)), "r"(bytes) : "memory");
 }
@@ -251,13 +254,7 @@ __device__ __forceinline__ void tma_load(void* dst, const TmaDesc* m, int x, int
   asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
                :: "r"(sa(dst)), "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(sa(b)) : "memory");
 }
-__device__ __forceinline__ void tma_store(const TmaDesc* m, const void* src, int x, int y, int z, int w) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
-               :: "l"(m), "r"(sa(src)), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ u32 smid() { u32 r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 // 32 values per lane -> lane L returns the warp sum of v[L] (31 shuffles)
 __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 #pragma unroll
@@ -272,37 +269,113 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   }
   return v[0];
 }
+// Work scheduler (thread 0 only): per-table atomic counters handing out sets of
+// PPC consecutive planes; a CTA starts on its SM's home table (so co-resident
+// warps share one specialised code path in the instruction cache) and moves on
+// to the next table when it is exhausted.  `raw` is a counter value fetched one
+// set ahead, so the atomic's latency is hidden behind a whole set of compute.
+__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
+  while (tcur >= 0) {
+    if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
+    if (++tried >= NT) { tcur = -1; break; }
+    tcur = tcur + 1 == NT ? 0 : tcur + 1;
+    raw = atomicAdd(sched + tcur, (unsigned)PPC);
+  }
+  return -1;
+}
+__device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
+  if (tcur >= 0) raw = atomicAdd(sched + tcur, (unsigned)PPC);
+}
+// item of plane slot q of a set whose first item is `base` (-1 when past the table's end)
+__device__ __forceinline__ int slot_item(int base, int q) {
+  if (base < 0) return -1;
+  const int t = base >> 22, i = (base & 0x3FFFFF) + q;
+  return i < COUNT[t] ? ((t << 22) | i) : -1;
+}
+__device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
+  t = item >> 22;
+  const int i = item & 0x3FFFFF;
+  c = CHLIST[CHOFF[t] + i / NB];
+  n = i - (i / NB) * NB;
+}
+__device__ __forceinline__ void sched_exit(unsigned* sched) {
+  __threadfence();
+  if (atomicAdd(sched + NT, 1u) == gridDim.x - 1) {
+    for (int t = 0; t < NT; ++t) sched[t] = 0u;
+    sched[NT] = 0u;
+    __threadfence();
+  }
+}
 )";
 
 struct Ctx {
-    int N, C, K, Ho, Wo, BR, BC, nthreads, nwarps, nt;
-    int sdy_pitch;
+    int N, C, K, Ho, Wo, BR, BC, wpg, G, PPC, nt, nsm;  // wpg: warps per tap group; G: tap groups; PPC: planes per CTA
+    int nthreads() const { return 32 * wpg * G * PPC; }
+    int wpp() const { return wpg * G; }  // warps per plane slot
 };
 
-void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of) {
-    os << "#define NT " << x.nt << "\n" << kPrelude;
-    os << "__constant__ unsigned char TABLE_OF[" << x.C << "] = {";
-    for (int c = 0; c < x.C; ++c) os << (c ? "," : "") << table_of[c];
+void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
+    os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define PPC " << x.PPC << "\n";
+    os << "__constant__ int COUNT[" << x.nt << "] = {";
+    for (int t = 0; t < x.nt; ++t) os << (t ? "," : "") << count[t];
     os << "};\n";
+    std::vector<int> choff(x.nt + 1, 0), chlist;
+    for (int t = 0; t < x.nt; ++t) {
+        choff[t] = (int)chlist.size();
+        for (int c = 0; c < x.C; ++c)
+            if (table_of[c] == t) chlist.push_back(c);
+    }
+    choff[x.nt] = (int)chlist.size();
+    os << "__constant__ int CHOFF[" << x.nt + 1 << "] = {";
+    for (int t = 0; t <= x.nt; ++t) os << (t ? "," : "") << choff[t];
+    os << "};\n__constant__ short CHLIST[" << x.C << "] = {";
+    for (int c = 0; c < x.C; ++c) os << (c ? "," : "") << chlist[c];
+    os << "};\n";
+    // home table per SM: SMs split among tables in proportion to their planes
+    long total = 0;
+    for (int t = 0; t < x.nt; ++t) total += count[t];
+    os << "__constant__ unsigned char HOME[" << x.nsm << "] = {";
+    long acc = 0;
+    int t = 0;
+    for (int s = 0; s < x.nsm; ++s) {
+        const double pos = (s + 0.5) * (double)total / x.nsm;
+        while (t < x.nt - 1 && pos >= acc + count[t]) acc += count[t], ++t;
+        os << (s ? "," : "") << t;
+    }
+    os << "};\n" << kPrelude;
 }
 
-// thread -> 7x7 block map: lanes cover 8 block-columns x 4 block-rows
+// thread -> (plane slot, tap group, 7x7 block): lanes cover 8 block-columns x 4 block-rows
 void emit_thread_map(std::ostringstream &os, const Ctx &x) {
     const int bcg = (x.BC + 7) / 8;
     os << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
-       << "  int bc = (lane & 7) + 8 * (warp % " << bcg << "), br = (lane >> 3) + 4 * (warp / " << bcg << ");\n"
+       << "  const int pp = warp / " << x.wpp() << ", grp = (warp / " << x.wpg << ") % " << x.G
+       << ", wg = warp % " << x.wpg << ";\n"
+       << "  const int ptid = tid - pp * " << 32 * x.wpp() << ";  // thread index within the plane slot\n"
+       << "  int bc = (lane & 7) + 8 * (wg % " << bcg << "), br = (lane >> 3) + 4 * (wg / " << bcg << ");\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n";
 }
 
-// For each footprint row i (relative to the block's top row), the (r, tap) pairs
-// reading it; emit one LDS per needed input pixel and the FMAs that consume it.
+// distinct taps of tap group gi (contiguous ranges of the distinct-tap list)
+std::vector<int> group_taps(const Geo &g, int gi, int G) {
+    const int nd = (int)g.taps.size();
+    std::vector<int> v;
+    for (int d = (gi * nd) / G; d < ((gi + 1) * nd) / G; ++d) v.push_back(d);
+    return v;
+}
+
+// For each footprint pixel (row i, col j relative to the block's top-left) of the
+// taps `ds`, the (distinct tap, r, s) uses: one LDS per needed input pixel, then
+// the FMAs that consume it (the register-blocked form of Def. 1's sum over k).
 template <typename F>
-void for_each_pixel(const Geo &g, F &&f) {
-    for (int i = g.minDH; i <= g.maxDH + R - 1; ++i) {
+void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
+    int lo_h = 1 << 20, hi_h = -(1 << 20);
+    for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
+    for (int i = lo_h; i <= hi_h + R - 1; ++i) {
         std::vector<std::pair<int, int>> pairs;  // (r, distinct tap)
         for (int r = 0; r < R; ++r)
-            for (int d = 0; d < (int)g.taps.size(); ++d)
+            for (int d : ds)
                 if (g.taps[d].dh == i - r) pairs.push_back({r, d});
         if (pairs.empty()) continue;
         int lo = 1 << 20, hi = -(1 << 20);
@@ -322,152 +395,320 @@ void for_each_pixel(const Geo &g, F &&f) {
     }
 }
 
-void emit_weights(std::ostringstream &os, const Geo &g, int K) {
-    for (int k = 0; k < K; ++k) os << "    const float w" << k << " = __ldg(wp + " << k << ");\n";
-    for (int d = 0; d < (int)g.taps.size(); ++d) {
-        os << "    const float m" << d << " = ";
-        for (size_t i = 0; i < g.taps[d].ks.size(); ++i) os << (i ? " + " : "") << "w" << g.taps[d].ks[i];
-        os << ";\n";
-    }
+size_t tile_bytes_of(const std::vector<Geo> &geo) {
+    size_t b = 0;
+    for (auto &g : geo) b = std::max(b, (size_t)g.bytes);
+    return (b + 1023) & ~(size_t)1023;
 }
 
-std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of) {
-    std::ostringstream os;
-    emit_header(os, x, table_of);
-    size_t tile_bytes = (size_t)x.Ho * x.Wo * 4;
-    for (auto &g : geo) tile_bytes = std::max(tile_bytes, (size_t)g.bytes);
-    tile_bytes = (tile_bytes + 127) & ~(size_t)127;
-    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads << ") o1d_stencil(const __grid_constant__ Params p) {\n"
-       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
-       << "  float* tile = reinterpret_cast<float*>(smem);\n"
-       << "  u64* bar = reinterpret_cast<u64*>(smem + " << tile_bytes << ");\n"
-       << "  const int c = blockIdx.x / " << x.N << ", n = blockIdx.x - c * " << x.N << ";\n"
-       << "  const int t = TABLE_OF[c];\n";
-    emit_thread_map(os, x);
-    os << "  if (tid == 0) {\n    mbar_init(bar, 1);\n    switch (t) {\n";
+size_t stage_bytes_of(const Ctx &x) { return ((size_t)x.Ho * x.Wo * 4 + 1023) & ~(size_t)1023; }
+
+// Shared-memory layout (both kernels):
+//   tiles [2 sets][PPC] | stage [PPC] (stencil only) | wsm [2][PPC][64] | bar [2] | s_item [2][PPC] | red
+struct Layout {
+    size_t TB, tiles, stage, wsm, bar, sitem, red, total;
+};
+Layout layout_of(const Ctx &x, const std::vector<Geo> &geo, bool stage, size_t red_bytes) {
+    Layout L;
+    L.TB = tile_bytes_of(geo);
+    L.tiles = 0;
+    L.stage = 2 * x.PPC * L.TB;
+    L.wsm = L.stage + (stage ? x.PPC * stage_bytes_of(x) : 0);
+    L.bar = L.wsm + 2 * x.PPC * 64 * 4;
+    L.sitem = L.bar + 16;
+    L.red = (L.sitem + 8 * x.PPC + 15) & ~(size_t)15;
+    L.total = L.red + red_bytes;
+    return L;
+}
+
+// Scheduling block run by warp 0 once the CTA finished reading buffer set b:
+// resolve the prefetched counter into the next set of PPC items, stage their
+// weights and issue their TMA loads (one mbarrier per set).
+void emit_schedule(std::ostringstream &os, const Ctx &x, const std::vector<Geo> &geo, const Layout &L,
+                   const std::string &b, bool weights, const std::string &ind) {
+    os << ind << "if (warp == 0) {\n"
+       << ind << "  int base = -1;\n"
+       << ind << "  if (lane == 0) { base = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
+       << ind << "  base = __shfl_sync(0xffffffffu, base, 0);\n"
+       << ind << "  int* si = s_item + (" << b << ") * PPC;\n"
+       << ind << "  if (lane < PPC) si[lane] = slot_item(base, lane);\n"
+       << ind << "  if (base >= 0) {\n";
+    if (weights)
+        os << ind << "    for (int e = lane; e < PPC * " << x.K << "; e += 32) {\n"
+           << ind << "      const int q = e / " << x.K << ", k = e - q * " << x.K << ";\n"
+           << ind << "      const int itq = slot_item(base, q);\n"
+           << ind << "      if (itq >= 0) { int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
+           << ind << "        wsm[((" << b << ") * PPC + q) * 64 + k] = __ldg(p.w + cq * " << x.K << " + k); }\n"
+           << ind << "    }\n";
+    os << ind << "    if (lane == 0) {\n"
+       << ind << "      unsigned bytes = 0;\n"
+       << ind << "      for (int q = 0; q < PPC; ++q) { const int itq = slot_item(base, q); if (itq < 0) break;\n"
+       << ind << "        switch (itq >> 22) {\n";
+    for (int t = 0; t < x.nt; ++t) os << ind << "        case " << t << ": bytes += " << geo[t].bytes << "u; break;\n";
+    os << ind << "        }\n" << ind << "      }\n"
+       << ind << "      mbar_expect(bar + (" << b << "), bytes);\n"
+       << ind << "      for (int q = 0; q < PPC; ++q) { const int itq = slot_item(base, q); if (itq < 0) break;\n"
+       << ind << "        int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
+       << ind << "        float* dst = reinterpret_cast<float*>(smem + ((" << b << ") * PPC + q) * " << L.TB << ");\n"
+       << ind << "        switch (tq) {\n";
     for (int t = 0; t < x.nt; ++t)
-        os << "      case " << t << ": mbar_expect(bar, " << geo[t].bytes << "u); tma_load(tile, &p.in_map[" << t
-           << "], " << geo[t].x0 << ", " << geo[t].minDH << ", c, n, bar); break;\n";
-    os << "    }\n  }\n  const float* wp = p.w + c * " << x.K << ";\n";
-    os << "  switch (t) {\n";
+        os << ind << "        case " << t << ": tma_load(dst, &p.in_map[" << t << "], " << geo[t].x0 << ", "
+           << geo[t].minDH << ", cq, nq, bar + (" << b << ")); break;\n";
+    os << ind << "        }\n" << ind << "      }\n" << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
+}
+
+// prologue: barriers, the first two sets, their weights and TMA loads
+void emit_prologue(std::ostringstream &os, const Ctx &x, const std::vector<Geo> &geo, const Layout &L, bool weights) {
+    os << "  float* wsm = reinterpret_cast<float*>(smem + " << L.wsm << ");\n"
+       << "  u64* bar = reinterpret_cast<u64*>(smem + " << L.bar << ");\n"
+       << "  int* s_item = reinterpret_cast<int*>(smem + " << L.sitem << ");\n"
+       << "  int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "  if (tid == 0) {\n    mbar_init(bar, 1); mbar_init(bar + 1, 1); fence_mbar_init();\n"
+       << "    tcur = HOME[smid() % " << x.nsm << "];\n    raw = atomicAdd(p.sched + tcur, (unsigned)PPC);\n  }\n"
+       << "  __syncthreads();\n";
+    emit_schedule(os, x, geo, L, "0", weights, "  ");
+    emit_schedule(os, x, geo, L, "1", weights, "  ");
+    os << "  __syncthreads();\n";
+}
+
+std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
+                        const std::vector<int> &count) {
+    std::ostringstream os;
+    emit_header(os, x, table_of, count);
+    const Layout L = layout_of(x, geo, true, 0);
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
+    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads() << ") o1d_stencil(const __grid_constant__ Params p) {\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
+    emit_thread_map(os, x);
+    emit_prologue(os, x, geo, L, true);
+    os << "  float* const stg = reinterpret_cast<float*>(smem + " << L.stage << " + pp * " << stage_bytes_of(x) << ");\n"
+       << "  float* const sto = stg + (" << R << " * br) * " << x.Wo << " + " << S << " * bc;\n"
+       << "  for (int it = 0;; ++it) {\n"
+       << "    const int b = it & 1;\n"
+       << "    if (s_item[b * PPC] < 0) break;\n"
+       << "    const int item = s_item[b * PPC + pp];\n"
+       << "    int cur[PPC];  // this set's items (s_item[b] is reused for the next set before the stores)\n"
+       << "    for (int q = 0; q < PPC; ++q) cur[q] = s_item[b * PPC + q];\n"
+       << "    int t = 0, c = 0, n = 0;\n"
+       << "    if (item >= 0) item_cn(item, t, c, n);\n"
+       << "    const float* tile = reinterpret_cast<const float*>(smem + (b * PPC + pp) * " << L.TB << ");\n"
+       << "    const float* wv = wsm + (b * PPC + pp) * 64;\n"
+       << "    mbar_wait(bar + b, (it >> 1) & 1);\n"
+       << "    if (tid == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+       << "    if (item < 0) {\n"
+       << "      __syncthreads();\n";
+    emit_schedule(os, x, geo, L, "b", true, "      ");
+    for (int gi = x.G - 1; gi > 0; --gi) os << "      __syncthreads();\n";
+    os << "    } else switch (t) {\n";
+    auto store_pred = [&](int r, int s) {
+        std::ostringstream q;
+        if (ragged) q << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
+        return q.str();
+    };
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
-        os << "  case " << t << ": {\n";
-        emit_weights(os, g, x.K);
+        os << "    case " << t << ": {\n";
         for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << " = 0.f;\n";
-        os << "    const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
-        os << "    __syncthreads();\n    mbar_wait(bar, 0);\n";
-        for_each_pixel(g, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-            os << "    { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
-            for (auto &u : uses) {
-                const int r = u.second.first, s = u.second.second;
-                os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
+            for (int s = 0; s < S; ++s) os << "      float a" << r << "_" << s << " = 0.f;\n";
+        os << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+        for (int gi = 0; gi < x.G; ++gi) {
+            const std::vector<int> ds = group_taps(g, gi, x.G);
+            os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
+               << "{\n";
+            for (int d : ds) {
+                os << "        const float m" << d << " = ";
+                for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
+                os << ";\n";
             }
-            os << " }\n";
-        });
-        os << "    __syncthreads();\n    if (active) {\n      float* o = tile + (" << R << " * br) * " << x.Wo << " + "
-           << S << " * bc;\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) {
-                os << "      ";
-                if (ragged) os << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s
-                               << " < " << x.Wo << ") ";
-                os << "o[" << r * x.Wo + s << "] = a" << r << "_" << s << ";\n";
-            }
-        os << "    }\n    break;\n  }\n";
+            for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+                os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                for (auto &u : uses) {
+                    const int r = u.second.first, s = u.second.second;
+                    os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
+                }
+                os << " }\n";
+            });
+            os << "      }\n";
+        }
+        // combine the tap groups in a fixed order through the staging tile:
+        // y = ((acc_{G-1}) + acc_{G-2}) + ... + acc_0
+        os << "      __syncthreads();\n";
+        emit_schedule(os, x, geo, L, "b", true, "      ");
+        for (int gi = x.G - 1; gi >= 0; --gi) {
+            os << "      if (grp == " << gi << " && active) {\n";
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) {
+                    os << "        " << store_pred(r, s) << "sto[" << r * x.Wo + s << "] = ";
+                    if (gi == x.G - 1)
+                        os << "a" << r << "_" << s << ";\n";
+                    else
+                        os << "sto[" << r * x.Wo + s << "] + a" << r << "_" << s << ";\n";
+                }
+            os << "      }\n";
+            if (gi > 0) os << "      __syncthreads();\n";
+        }
+        os << "      break;\n    }\n";
     }
-    os << "  }\n  fence_async_smem();\n  __syncthreads();\n"
-       << "  if (tid == 0) tma_store(&p.aux_map, tile, 0, 0, c, n);\n}\n";
+    os << "    }\n"
+       << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+       << "    __syncthreads();\n"
+       << "    if (tid == 0) {\n"
+       << "      for (int q = 0; q < PPC; ++q) {\n"
+       << "        const int itq = cur[q];\n"
+       << "        if (itq < 0) break;\n"
+       << "        int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
+       << "        asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
+       << "                     :: \"l\"(&p.out_map), \"r\"(sa(smem + " << L.stage << " + q * " << stage_bytes_of(x)
+       << ")), \"r\"(0), \"r\"(0), \"r\"(cq), \"r\"(nq) : \"memory\");\n"
+       << "      }\n"
+       << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+       << "    }\n"
+       << "  }\n"
+       << "  if (tid == 0) { asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\"); sched_exit(p.sched); }\n}\n";
     return os.str();
 }
 
-std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of) {
+int wgrad_rounds(const Ctx &x, const std::vector<Geo> &geo) {
+    int maxslots = 0;
+    for (auto &g : geo)
+        for (int gi = 0; gi < x.G; ++gi) maxslots = std::max(maxslots, (int)group_taps(g, gi, x.G).size());
+    return (maxslots + 31) / 32;
+}
+
+size_t red_bytes(const Ctx &x, const std::vector<Geo> &geo) {
+    return 4 * 32 * wgrad_rounds(x, geo) * x.wpg * x.G * x.PPC;
+}
+
+std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
+                      const std::vector<int> &count) {
     std::ostringstream os;
-    emit_header(os, x, table_of);
-    size_t tile_bytes = 0;
-    for (auto &g : geo) tile_bytes = std::max(tile_bytes, (size_t)g.bytes);
-    tile_bytes = (tile_bytes + 1023) & ~(size_t)1023;
-    const size_t dy_bytes = ((size_t)R * x.BR * x.sdy_pitch * 4 + 127) & ~(size_t)127;
-    const int rounds = (x.K + 31) / 32;
-    os << "__constant__ unsigned char K2D[" << x.nt << "][" << x.K << "] = {";
+    emit_header(os, x, table_of, count);
+    const Layout L = layout_of(x, geo, false, red_bytes(x, geo));
+    const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
+    const int rounds = wgrad_rounds(x, geo);
+    std::vector<std::vector<int>> k2g(x.nt, std::vector<int>(x.K)), k2s(x.nt, std::vector<int>(x.K));
+    for (int t = 0; t < x.nt; ++t)
+        for (int gi = 0; gi < x.G; ++gi) {
+            const std::vector<int> ds = group_taps(geo[t], gi, x.G);
+            for (int k = 0; k < x.K; ++k)
+                for (size_t q = 0; q < ds.size(); ++q)
+                    if (geo[t].k2d[k] == ds[q]) k2g[t][k] = gi, k2s[t][k] = (int)q;
+        }
+    os << "__constant__ unsigned char K2G[" << x.nt << "][" << x.K << "] = {";
     for (int t = 0; t < x.nt; ++t) {
         os << (t ? "," : "") << "{";
-        for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << geo[t].k2d[k];
+        for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << k2g[t][k];
+        os << "}";
+    }
+    os << "};\n__constant__ unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
+    for (int t = 0; t < x.nt; ++t) {
+        os << (t ? "," : "") << "{";
+        for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << k2s[t][k];
         os << "}";
     }
     os << "};\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
-       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
-       << "  float* tile = reinterpret_cast<float*>(smem);\n"
-       << "  float* sdy = reinterpret_cast<float*>(smem + " << tile_bytes << ");\n"
-       << "  float* red = reinterpret_cast<float*>(smem + " << tile_bytes + dy_bytes << ");\n"
-       << "  u64* bar = reinterpret_cast<u64*>(smem + " << tile_bytes + dy_bytes + 4 * 32 * rounds * x.nwarps << ");\n"
-       << "  __shared__ int s_last;\n"
-       << "  const int c = blockIdx.x / " << x.N << ", n = blockIdx.x - c * " << x.N << ";\n"
-       << "  const int t = TABLE_OF[c];\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads() << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
     emit_thread_map(os, x);
-    os << "  if (tid == 0) {\n    mbar_init(bar, 1);\n    switch (t) {\n";
-    const uint32_t dyb = (uint32_t)(R * x.BR * x.sdy_pitch * 4);
-    for (int t = 0; t < x.nt; ++t)
-        os << "      case " << t << ": mbar_expect(bar, " << geo[t].bytes + dyb << "u); tma_load(tile, &p.in_map[" << t
-           << "], " << geo[t].x0 << ", " << geo[t].minDH << ", c, n, bar); break;\n";
-    os << "    }\n    tma_load(sdy, &p.aux_map, 0, 0, c, n, bar);\n  }\n";
+    emit_prologue(os, x, geo, L, false);
+    os << "  float* red = reinterpret_cast<float*>(smem + " << L.red << ");\n"
+       << "  const float* const dyp = reinterpret_cast<const float*>(p.io);\n";
+    auto emit_dy_load = [&](const char *dst, const char *itemexpr) {
+        os << "    {\n      const int itm = " << itemexpr << ";\n"
+           << "      if (itm >= 0 && active) {\n        int tt, cc, nn; item_cn(itm, tt, cc, nn);\n"
+           << "        const float* gp = dyp + ((u64)(nn * " << x.C << " + cc) * " << x.Ho << " + " << R << " * br) * "
+           << x.Wo << " + " << S << " * bc;\n";
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+                os << "        " << dst << r << "_" << s << " = ";
+                if (ragged)
+                    os << "(" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < "
+                       << x.Wo << ") ? __ldg(gp + " << r * x.Wo + s << ") : 0.f;\n";
+                else
+                    os << "__ldg(gp + " << r * x.Wo + s << ");\n";
+            }
+        os << "      } else {\n";
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) os << "        " << dst << r << "_" << s << " = 0.f;\n";
+        os << "      }\n    }\n";
+    };
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) os << "  float g" << r << "_" << s << ", h" << r << "_" << s << ";\n";
+    emit_dy_load("g", "s_item[pp]");
     os << "  float v0[32]";
     for (int rd = 1; rd < rounds; ++rd) os << ", v" << rd << "[32]";
-    os << ";\n  __syncthreads();\n  mbar_wait(bar, 0);\n";
-    os << "  const float* gb = sdy + (" << R << " * br) * " << x.sdy_pitch << " + " << S << " * bc;\n";
-    for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s)
-            os << "  const float g" << r << "_" << s << " = active ? gb[" << r * x.sdy_pitch + s << "] : 0.f;\n";
-    os << "  switch (t) {\n";
+    os << ";\n  for (int it = 0;; ++it) {\n"
+       << "    const int b = it & 1;\n"
+       << "    if (s_item[b * PPC] < 0) break;\n"
+       << "    const int item = s_item[b * PPC + pp];\n"
+       << "    int t = 0, c = 0, n = 0;\n"
+       << "    if (item >= 0) item_cn(item, t, c, n);\n";
+    emit_dy_load("h", "s_item[(b ^ 1) * PPC + pp]");  // prefetch the next set's dy (its tiles are in flight)
+    os << "    const float* tile = reinterpret_cast<const float*>(smem + (b * PPC + pp) * " << L.TB << ");\n"
+       << "    mbar_wait(bar + b, (it >> 1) & 1);\n";
+    for (int rd = 0; rd < rounds; ++rd)
+        os << "    for (int q = 0; q < 32; ++q) v" << rd << "[q] = 0.f;\n";
+    os << "    if (item >= 0) switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
-        const int nd = (int)g.taps.size();
-        os << "  case " << t << ": {\n";
-        for (int d = 0; d < nd; ++d) os << "    float q" << d << " = 0.f;\n";
-        os << "    const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
-        for_each_pixel(g, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-            os << "    { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
-            for (auto &u : uses)
-                os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", v, q" << u.first
-                   << ");";
-            os << " }\n";
-        });
-        for (int d = 0; d < 32 * rounds; ++d)
-            os << "    v" << d / 32 << "[" << d % 32 << "] = " << (d < nd ? "q" + std::to_string(d) : "0.f") << ";\n";
-        os << "    break;\n  }\n";
+        os << "    case " << t << ": {\n"
+           << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+        for (int gi = 0; gi < x.G; ++gi) {
+            const std::vector<int> ds = group_taps(g, gi, x.G);
+            os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
+               << "{\n";
+            for (int d : ds) os << "        float q" << d << " = 0.f;\n";
+            for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+                os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                for (auto &u : uses)
+                    os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", v, q"
+                       << u.first << ");";
+                os << " }\n";
+            });
+            for (size_t q = 0; q < ds.size(); ++q) os << "        v" << q / 32 << "[" << q % 32 << "] = q" << ds[q] << ";\n";
+            os << "      }\n";
+        }
+        os << "      break;\n    }\n";
     }
-    os << "  }\n";
+    os << "    }\n";
     for (int rd = 0; rd < rounds; ++rd)
-        os << "  red[warp * " << 32 * rounds << " + " << 32 * rd << " + lane] = reduce_scatter32(v" << rd << ", lane);\n";
-    os << "  __syncthreads();\n"
-       << "  float* wsp = p.ws + (u64)blockIdx.x * " << x.K << ";\n"
-       << "  if (tid < " << x.K << ") {\n    const int d = K2D[t][tid];\n    float s = 0.f;\n"
-       << "    for (int w = 0; w < " << x.nwarps << "; ++w) s += red[w * " << 32 * rounds << " + d];\n"
-       << "    wsp[tid] = s;\n  }\n"
-       << "  __threadfence();\n  __syncthreads();\n"
-       << "  if (tid == 0) {\n    const unsigned old = atomicAdd(p.cnt + c, 1u);\n"
-       << "    s_last = ((old + 1u) % " << x.N << "u) == 0u;\n  }\n  __syncthreads();\n"
-       << "  if (s_last) {\n    __threadfence();\n"
-       << "    for (int k = tid; k < " << x.K << "; k += " << x.nthreads << ") {\n      double s = 0.0;\n"
-       << "      const float* col = p.ws + (u64)c * " << x.N << " * " << x.K << " + k;\n"
-       << "      for (int i = 0; i < " << x.N << "; ++i) s += (double)__ldcg(col + (u64)i * " << x.K << ");\n"
-       << "      p.dW[c * " << x.K << " + k] = (float)s;\n    }\n  }\n}\n";
+        os << "    red[warp * " << 32 * rounds << " + " << 32 * rd << " + lane] = reduce_scatter32(v" << rd
+           << ", lane);\n";
+    os << "    __syncthreads();\n";
+    emit_schedule(os, x, geo, L, "b", false, "    ");
+    os << "    if (item >= 0) {\n"
+       << "      float* wsp = p.ws + (u64)(c * " << x.N << " + n) * " << x.K << ";\n"
+       << "      for (int k = ptid; k < " << x.K << "; k += " << 32 * x.wpp() << ") {\n"
+       << "        const float* rp = red + ((pp * " << x.G << " + K2G[t][k]) * " << x.wpg << ") * " << 32 * rounds
+       << " + K2S[t][k];\n"
+       << "        float s = 0.f;\n"
+       << "        for (int w = 0; w < " << x.wpg << "; ++w) s += rp[w * " << 32 * rounds << "];\n"
+       << "        wsp[k] = s;\n      }\n"
+       << "      __threadfence();\n    }\n"
+       << "    __syncthreads();\n"
+       << "    if (item >= 0 && warp == pp * " << x.wpp() << ") {\n      unsigned last = 0;\n"
+       << "      if (lane == 0) last = ((atomicAdd(p.cnt + c, 1u) + 1u) % " << x.N << "u) == 0u;\n"
+       << "      last = __shfl_sync(0xffffffffu, last, 0);\n"
+       << "      if (last) {\n        __threadfence();\n"
+       << "        for (int k = lane; k < " << x.K << "; k += 32) {\n          double s = 0.0;\n"
+       << "          const float* col = p.ws + (u64)c * " << x.N << " * " << x.K << " + k;\n"
+       << "#pragma unroll 8\n"
+       << "          for (int i = 0; i < " << x.N << "; ++i) s += (double)__ldcg(col + (u64)i * " << x.K << ");\n"
+       << "          p.dW[c * " << x.K << " + k] = (float)s;\n        }\n      }\n    }\n";
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) os << "    g" << r << "_" << s << " = h" << r << "_" << s << ";\n";
+    os << "  }\n  if (tid == 0) sched_exit(p.sched);\n}\n";
     return os.str();
 }
-
-// host mirror of the generated Params (layout must match the emitted struct)
-struct alignas(64) HostParamsHead {
-    CUtensorMap maps[1];
-};
-
-size_t params_size(int nt) { return sizeof(CUtensorMap) * (nt + 1) + 4 * sizeof(void *); }
 
 bool env_flag(const char *n) {
     const char *v = getenv(n);
     return v && *v && strcmp(v, "0") != 0;
+}
+
+int env_int(const char *n, int dflt) {
+    const char *v = getenv(n);
+    return (v && *v) ? atoi(v) : dflt;
 }
 
 o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH) {
@@ -488,39 +729,47 @@ o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int 
     return O1D_OK;
 }
 
-
 }  // namespace
 
 // Host-only part: eligibility, geometry and generated sources (no CUDA calls).
 // Returns false (and no sources) when the plan is not eligible.
-bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3]) {
+bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) {
     const o1d_desc &d = pl->d;
     if (d.stride != 1 || d.dtype != O1D_F32) return false;
     if ((d.W * 4) % 16 != 0 || d.K > 64) return false;
-    if (pl->n_distinct > 16) return false;
+    if (pl->n_distinct > 16 || (long)d.N * d.C >= (1L << 22)) return false;
     sp->BR = (pl->P + R - 1) / R;
     sp->BC = (pl->Q + S - 1) / S;
     const int bcg = (sp->BC + 7) / 8, brg = (sp->BR + 3) / 4;
-    sp->nwarps = bcg * brg;
-    sp->nthreads = 32 * sp->nwarps;
+    sp->wpg = bcg * brg;
+    sp->G = env_int("O1D_G", (sp->wpg <= 2 && d.K >= 8) ? 2 : 1);  // tap groups per plane
+    sp->PPC = env_int("O1D_PPC", 1);                                 // planes per CTA
+    if (sp->G < 1 || sp->G > 4 || sp->PPC < 1 || sp->PPC > 8) return false;
+    sp->nthreads = 32 * sp->wpg * sp->G * sp->PPC;
     sp->nt = pl->n_distinct;
-    sp->sdy_pitch = (S * sp->BC + 3) & ~3;
+    sp->nsm = nsm;
     std::vector<int> rep(sp->nt, -1);  // one representative channel per distinct table
-    for (int c = 0; c < d.C; ++c)
+    sp->count.assign(sp->nt, 0);
+    for (int c = 0; c < d.C; ++c) {
         if (rep[pl->table_of[c]] < 0) rep[pl->table_of[c]] = c;
+        sp->count[pl->table_of[c]] += d.N;
+    }
     for (int t = 0; t < sp->nt; ++t) {
         const int c = rep[t];
         sp->fwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, false, sp->BR, sp->BC, 4));
         sp->bwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, true, sp->BR, sp->BC, 4));
         for (const Geo *g : {&sp->fwd.back(), &sp->bwd.back()})
-            if (g->pitch > 256 || g->rows > 256 || g->bytes > 160 * 1024) return false;
+            if (g->pitch > 256 || g->rows > 256 || g->bytes > 100 * 1024) return false;
     }
     if (d.W > 256 || d.H > 256 || sp->nthreads > 1024) return false;
-    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->nthreads, sp->nwarps, sp->nt, sp->sdy_pitch};
+    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    for (const std::vector<Geo> *g : {&sp->fwd, &sp->bwd})
+        if (layout_of(x, *g, true, 0).total > 220 * 1024) return false;
+    if (layout_of(x, sp->fwd, false, red_bytes(x, sp->fwd)).total > 220 * 1024) return false;
     std::vector<int> table_of(pl->table_of.begin(), pl->table_of.end());
-    src[0] = gen_stencil(x, sp->fwd, table_of);
-    src[1] = gen_stencil(x, sp->bwd, table_of);
-    src[2] = gen_wgrad(x, sp->fwd, table_of);
+    src[0] = gen_stencil(x, sp->fwd, table_of, sp->count);
+    src[1] = gen_stencil(x, sp->bwd, table_of, sp->count);
+    src[2] = gen_wgrad(x, sp->fwd, table_of, sp->count);
     return true;
 }
 
@@ -529,9 +778,12 @@ o1d_status spec_create(o1d_plan *pl) {
     const o1d_desc &d = pl->d;
     Driver &dr = drv();
     if (!dr.err.empty()) return O1D_OK;  // no driver entry points: generic path
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pl->device) != cudaSuccess || nsm < 1)
+        return fail(O1D_CUDA_ERROR, "cannot query the SM count");
     SpecSet *sp = new SpecSet();
     std::string src[3];
-    if (!spec_prepare(pl, sp, src)) {
+    if (!spec_prepare(pl, sp, src, nsm)) {
         delete sp;
         return O1D_OK;
     }
@@ -559,47 +811,48 @@ o1d_status spec_create(o1d_plan *pl) {
             delete sp;
             return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
         }
-    // size the shared memory of each kernel (must match the emitted offsets)
-    size_t tile_f = (size_t)pl->P * pl->Q * 4, tile_b = tile_f, tile_w = 0;
-    for (auto &g : sp->fwd) tile_f = std::max(tile_f, (size_t)g.bytes), tile_w = std::max(tile_w, (size_t)g.bytes);
-    for (auto &g : sp->bwd) tile_b = std::max(tile_b, (size_t)g.bytes);
-    tile_f = (tile_f + 127) & ~(size_t)127;
-    tile_b = (tile_b + 127) & ~(size_t)127;
-    tile_w = (tile_w + 1023) & ~(size_t)1023;
-    const size_t dy_bytes = ((size_t)R * sp->BR * sp->sdy_pitch * 4 + 127) & ~(size_t)127;
-    sp->smem[0] = tile_f + 16;
-    sp->smem[1] = tile_b + 16;
-    sp->smem[2] = tile_w + dy_bytes + 4 * 32 * ((d.K + 31) / 32) * sp->nwarps + 16;
+    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    sp->smem[0] = layout_of(x, sp->fwd, true, 0).total;
+    sp->smem[1] = layout_of(x, sp->bwd, true, 0).total;
+    sp->smem[2] = layout_of(x, sp->fwd, false, red_bytes(x, sp->fwd)).total;
     const char *fnames[3] = {"o1d_stencil", "o1d_stencil", "o1d_wgrad"};
+    PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occ = nullptr;
+    std::string e;
+    entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", &occ, &e);
+    const long planes = ((long)d.N * d.C + sp->PPC - 1) / sp->PPC;
     for (int i = 0; i < 3; ++i) {
         CUresult r = dr.moduleLoadData(&sp->mod[i], cubin[i].data());
         if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&sp->fn[i], sp->mod[i], fnames[i]);
         if (r == CUDA_SUCCESS)
             r = dr.funcSetAttribute(sp->fn[i], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)sp->smem[i]);
-        if (r != CUDA_SUCCESS) {
+        int blocks = 0;
+        if (r == CUDA_SUCCESS && occ) r = occ(&blocks, sp->fn[i], sp->nthreads, sp->smem[i]);
+        if (r != CUDA_SUCCESS || blocks < 1) {
             for (int j = 0; j <= i; ++j)
                 if (sp->mod[j]) dr.moduleUnload(sp->mod[j]);
             delete sp;
-            return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") + cu_err(r));
+            return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") +
+                                            (r != CUDA_SUCCESS ? cu_err(r) : "zero occupancy"));
         }
-        // keep the ptxas register / spill line for describe()
+        sp->grid[i] = (int)std::min<long>(planes, (long)blocks * nsm);
         const std::string &lg = logs[i];
         size_t pos = lg.find("Used ");
         sp->regs[i] = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
     }
-    if (cudaMalloc(&sp->d_counters, sizeof(unsigned) * d.C) != cudaSuccess ||
-        cudaMemset(sp->d_counters, 0, sizeof(unsigned) * d.C) != cudaSuccess) {
+    const size_t nsched = 3 * (sp->nt + 1) + d.C;
+    if (cudaMalloc(&sp->d_sched, sizeof(unsigned) * nsched) != cudaSuccess ||
+        cudaMemset(sp->d_sched, 0, sizeof(unsigned) * nsched) != cudaSuccess) {
         for (int j = 0; j < 3; ++j) dr.moduleUnload(sp->mod[j]);
         delete sp;
-        return fail(O1D_CUDA_ERROR, "counter allocation failed");
+        return fail(O1D_CUDA_ERROR, "scheduler counter allocation failed");
     }
     pl->spec = sp;
-    char buf[512];
+    char buf[768];
     snprintf(buf, sizeof buf,
-             "spec(7x7 blocks, %d threads/plane, %d tap tables, TMA 4-D; fwd %zu B smem [%s]; bwd_in [%s]; "
-             "wgrad %zu B smem [%s])",
-             sp->nthreads, sp->nt, sp->smem[0], sp->regs[0].c_str(), sp->regs[1].c_str(), sp->smem[2],
-             sp->regs[2].c_str());
+             "spec(persistent, 7x7 blocks, %d threads/CTA (%d planes x %d tap groups), %d tap tables, TMA 4-D double-buffered; "
+             "fwd grid %d smem %zu [%s]; bwd_in grid %d [%s]; wgrad grid %d smem %zu [%s])",
+             sp->nthreads, sp->PPC, sp->G, sp->nt, sp->grid[0], sp->smem[0], sp->regs[0].c_str(), sp->grid[1], sp->regs[1].c_str(),
+             sp->grid[2], sp->smem[2], sp->regs[2].c_str());
     pl->describe = buf;
     if (env_flag("O1D_VERBOSE")) fprintf(stderr, "[o1d] %s\n", buf);
     return O1D_OK;
@@ -610,7 +863,7 @@ void spec_destroy(o1d_plan *pl) {
     if (!sp) return;
     for (int i = 0; i < 3; ++i)
         if (sp->mod[i]) drv().moduleUnload(sp->mod[i]);
-    if (sp->d_counters) cudaFree(sp->d_counters);
+    if (sp->d_sched) cudaFree(sp->d_sched);
     delete sp;
     pl->spec = nullptr;
 }
@@ -627,31 +880,29 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const int nt = sp->nt;
-    std::vector<unsigned char> blob(params_size(nt) + 64);
-    unsigned char *base = blob.data();
-    base += (64 - (reinterpret_cast<uintptr_t>(base) & 63)) & 63;
-    CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(base);
+    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 6 * sizeof(void *)];
+    CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(blob);
     const std::vector<Geo> &geo = pass == 1 ? sp->bwd : sp->fwd;
-    // input maps: x for forward / wgrad, dy for backward_input; per table box
+    // input maps (x for forward / wgrad, dy for backward_input), one box per table
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
     for (int t = 0; t < nt; ++t)
         if (o1d_status st = encode(&maps[t], a, d.dtype, inW, inH, d.C, d.N, geo[t].pitch, geo[t].rows)) return st;
-    if (pass == 2) {
-        // dy (b) staged as a zero-padded 7*BR x sdy_pitch box
-        if (o1d_status st = encode(&maps[nt], b, d.dtype, pl->Q, pl->P, d.C, d.N, sp->sdy_pitch, R * sp->BR)) return st;
-    } else {
+    if (pass != 2) {  // dense output box for the TMA store
         const int oW = pass == 1 ? d.W : pl->Q, oH = pass == 1 ? d.H : pl->P;
         if (o1d_status st = encode(&maps[nt], b, d.dtype, oW, oH, d.C, d.N, oW, oH)) return st;
+    } else {
+        memset(&maps[nt], 0, sizeof(CUtensorMap));
     }
-    void **ptrs = reinterpret_cast<void **>(base + sizeof(CUtensorMap) * (nt + 1));
+    void **ptrs = reinterpret_cast<void **>(blob + sizeof(CUtensorMap) * (nt + 1));
     ptrs[0] = const_cast<float *>(w);
-    ptrs[1] = ws;
-    ptrs[2] = sp->d_counters;
-    ptrs[3] = dW;
-    void *args[] = {base};
-    const unsigned grid = (unsigned)(d.N * d.C);
-    CUresult r = drv().launchKernel(sp->fn[pass], grid, 1, 1, sp->nthreads, 1, 1, (unsigned)sp->smem[pass],
-                                    static_cast<CUstream>(stream), args, nullptr);
+    ptrs[1] = const_cast<void *>(b);
+    ptrs[2] = ws;
+    ptrs[3] = sp->d_sched + pass * (nt + 1);
+    ptrs[4] = sp->d_sched + 3 * (nt + 1);
+    ptrs[5] = dW;
+    void *args[] = {blob};
+    CUresult r = drv().launchKernel(sp->fn[pass], (unsigned)sp->grid[pass], 1, 1, sp->nthreads, 1, 1,
+                                    (unsigned)sp->smem[pass], static_cast<CUstream>(stream), args, nullptr);
     if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of specialised kernel: " + cu_err(r));
     return O1D_OK;
 }
@@ -660,7 +911,7 @@ o1d_status spec_source(const o1d_plan *pl, int pass, std::string *out) {
     SpecSet sp;
     std::string src[3];
     if (pass < 0 || pass > 2) return fail(O1D_INVALID_ARG, "pass must be 0, 1 or 2");
-    if (!spec_prepare(pl, &sp, src)) return fail(O1D_UNSUPPORTED, "plan is not eligible for specialised kernels");
+    if (!spec_prepare(pl, &sp, src, 148)) return fail(O1D_UNSUPPORTED, "plan is not eligible for specialised kernels");
     *out = src[pass];
     return O1D_OK;
 }
