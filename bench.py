@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--flags", type=int, default=0, help="o1d_desc.flags (1 = force generic kernels)")
+    ap.add_argument("--angle", type=float, default=None,
+                    help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
+    ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary bf16 measurement")
@@ -191,7 +194,12 @@ def run_ours(args):
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.dtype]
     es = 4 if args.dtype == "f32" else 2
     wl = inputs.S1
+    if args.dirs is not None:
+        from dataclasses import replace
+        wl = replace(wl, D=args.dirs)
     angles = B.direction_angles(wl.D, wl.C, wl.assign)
+    if args.angle is not None:
+        angles = np.full(wl.C, float(args.angle))
     plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, angles, dtype=tdt, flags=args.flags, device=dev)
     # two rotating buffer sets so every pass streams from HBM (each set 4 x 77 MB > L2)
     sets = []
@@ -300,7 +308,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64 U[-1,1))",
         "config": {"workload": wl.name, "N_per_gpu": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
-                   "angles": f"D={wl.D} {wl.assign}", "stride": 1, "layout": "NCHW",
+                   "angles": f"D={wl.D} {wl.assign}" if args.angle is None else f"all {args.angle} deg",
+                   "stride": 1, "layout": "NCHW",
                    "parallelism": f"dp{world} (batch-sharded, NCCL all-reduce of dW)",
                    "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -31,6 +31,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -254,6 +255,11 @@ __device__ __forceinline__ void tma_load(void* dst, const TmaDesc* m, int x, int
   asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
                :: "r"(sa(dst)), "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(sa(b)) : "memory");
 }
+__device__ __forceinline__ u64 f2pack(float lo, float hi) { u64 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r; }
+__device__ __forceinline__ float f2lo(u64 v) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); return lo; }
+__device__ __forceinline__ float f2hi(u64 v) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); return hi; }
+// packed fp32 FMA (two lanes per instruction, each fma.rn): d = a * b + c
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) { u64 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
 __device__ __forceinline__ u32 smid() { u32 r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 // 32 values per lane -> lane L returns the warp sum of v[L] (31 shuffles)
 __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
@@ -274,6 +280,29 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 // warps share one specialised code path in the instruction cache) and moves on
 // to the next table when it is exhausted.  `raw` is a counter value fetched one
 // set ahead, so the atomic's latency is hidden behind a whole set of compute.
+#ifdef GLOBAL_QUEUE
+// One queue over all planes in table-major order: at any moment the whole GPU
+// works on (at most two) consecutive tap tables, so the instruction footprint
+// in flight is one specialised code path, not NT of them.
+__device__ __forceinline__ int global_item(int g) {
+  int t = 0;
+  while (t < NT - 1 && g >= COUNT[t]) { g -= COUNT[t]; ++t; }
+  return (t << 22) | g;
+}
+__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
+  if (tcur < 0) return -1;
+  if (raw < (unsigned)TOTAL) return (int)raw;
+  tcur = -1;
+  return -1;
+}
+__device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
+  if (tcur >= 0) raw = atomicAdd(sched, (unsigned)PPC);
+}
+__device__ __forceinline__ int slot_item(int base, int q) {
+  if (base < 0 || base + q >= TOTAL) return -1;
+  return global_item(base + q);
+}
+#else
 __device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
   while (tcur >= 0) {
     if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
@@ -292,6 +321,7 @@ __device__ __forceinline__ int slot_item(int base, int q) {
   const int t = base >> 22, i = (base & 0x3FFFFF) + q;
   return i < COUNT[t] ? ((t << 22) | i) : -1;
 }
+#endif
 __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   t = item >> 22;
   const int i = item & 0x3FFFFF;
@@ -308,14 +338,31 @@ __device__ __forceinline__ void sched_exit(unsigned* sched) {
 }
 )";
 
+bool env_flag(const char *n) {
+    const char *v = getenv(n);
+    return v && *v && strcmp(v, "0") != 0;
+}
+
+int env_int(const char *n, int dflt) {
+    const char *v = getenv(n);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
 struct Ctx {
     int N, C, K, Ho, Wo, BR, BC, wpg, G, PPC, nt, nsm;  // wpg: warps per tap group; G: tap groups; PPC: planes per CTA
+    bool ffma2 = false;                                  // packed fp32 FMA in the stencil
     int nthreads() const { return 32 * wpg * G * PPC; }
     int wpp() const { return wpg * G; }  // warps per plane slot
 };
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
     os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define PPC " << x.PPC << "\n";
+    {
+        long tot = 0;
+        for (int t = 0; t < x.nt; ++t) tot += count[t];
+        os << "#define TOTAL " << tot << "\n";
+        if (env_int("O1D_HOME_MODE", 2) == 3) os << "#define GLOBAL_QUEUE 1\n";
+    }
     os << "__constant__ int COUNT[" << x.nt << "] = {";
     for (int t = 0; t < x.nt; ++t) os << (t ? "," : "") << count[t];
     os << "};\n";
@@ -335,12 +382,25 @@ void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &t
     long total = 0;
     for (int t = 0; t < x.nt; ++t) total += count[t];
     os << "__constant__ unsigned char HOME[" << x.nsm << "] = {";
+    const int mode = env_int("O1D_HOME_MODE", 2);
     long acc = 0;
     int t = 0;
     for (int s = 0; s < x.nsm; ++s) {
-        const double pos = (s + 0.5) * (double)total / x.nsm;
-        while (t < x.nt - 1 && pos >= acc + count[t]) acc += count[t], ++t;
-        os << (s ? "," : "") << t;
+        // mode 0: contiguous smid ranges per table, proportional to the table's planes;
+        // mode 1: smid mod NT; mode 2: (smid / 2) mod NT (TPC pairs)
+        int h;
+        if (mode == 3) {
+            h = 0;  // global table-major queue
+        } else if (mode == 1) {
+            h = s % x.nt;
+        } else if (mode == 2) {
+            h = (s / 2) % x.nt;
+        } else {
+            const double pos = (s + 0.5) * (double)total / x.nsm;
+            while (t < x.nt - 1 && pos >= acc + count[t]) acc += count[t], ++t;
+            h = t;
+        }
+        os << (s ? "," : "") << h;
     }
     os << "};\n" << kPrelude;
 }
@@ -471,6 +531,75 @@ void emit_prologue(std::ostringstream &os, const Ctx &x, const std::vector<Geo> 
     os << "  __syncthreads();\n";
 }
 
+// Stencil taps of group `ds` with packed FFMA2: output columns are paired
+// (s, s+1) so that the pixel pair starts at an even column relative to the
+// block: taps with even dw accumulate into pairs (0,1),(2,3),(4,5) + scalar 6
+// (set A), taps with odd dw into pairs (1,2),(3,4),(5,6) + scalar 0 (set B).
+// Every pixel pair is then an even-aligned (v_j, v_j+1) register pair.  The
+// two sets are added at the end: a_rs = A_rs + B_rs.
+void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, const char *ind) {
+    for (int d : ds) {
+        os << ind << "const float m" << d << " = ";
+        for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
+        os << ";\n" << ind << "const u64 M" << d << " = f2pack(m" << d << ", m" << d << ");\n";
+    }
+    for (int r = 0; r < R; ++r)
+        os << ind << "u64 A" << r << "_0 = 0ull, A" << r << "_2 = 0ull, A" << r << "_4 = 0ull; float A" << r
+           << "_6 = 0.f;\n"
+           << ind << "u64 B" << r << "_1 = 0ull, B" << r << "_3 = 0ull, B" << r << "_5 = 0ull; float B" << r
+           << "_0 = 0.f;\n";
+    int lo_h = 1 << 20, hi_h = -(1 << 20);
+    for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
+    auto vname = [](int j) { return std::string("v") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
+    auto pname = [](int j) { return std::string("P") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
+    for (int i = lo_h; i <= hi_h + R - 1; ++i) {
+        std::vector<std::pair<int, int>> pairs;  // (r, d)
+        for (int r = 0; r < R; ++r)
+            for (int d : ds)
+                if (g.taps[d].dh == i - r) pairs.push_back({r, d});
+        if (pairs.empty()) continue;
+        std::set<int> scal, pr;
+        for (auto &p : pairs) {
+            const int dw = g.taps[p.second].dw;
+            if (((dw % 2) + 2) % 2 == 0) {
+                for (int s = 0; s < 6; s += 2) pr.insert(dw + s);
+                scal.insert(dw + 6);
+            } else {
+                for (int s = 1; s < 7; s += 2) pr.insert(dw + s);
+                scal.insert(dw);
+            }
+        }
+        std::set<int> need(scal);
+        for (int j : pr) need.insert(j), need.insert(j + 1);
+        os << ind << "{\n";
+        for (int j : need)
+            os << ind << "  const float " << vname(j) << " = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];\n";
+        for (int j : pr) os << ind << "  const u64 " << pname(j) << " = f2pack(" << vname(j) << ", " << vname(j + 1) << ");\n";
+        for (auto &p : pairs) {
+            const int r = p.first, d = p.second, dw = g.taps[d].dw;
+            if (((dw % 2) + 2) % 2 == 0) {
+                for (int s = 0; s < 6; s += 2)
+                    os << ind << "  A" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
+                os << ind << "  A" << r << "_6 = fmaf(" << vname(dw + 6) << ", m" << d << ", A" << r << "_6);\n";
+            } else {
+                for (int s = 1; s < 7; s += 2)
+                    os << ind << "  B" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
+                os << ind << "  B" << r << "_0 = fmaf(" << vname(dw) << ", m" << d << ", B" << r << "_0);\n";
+            }
+        }
+        os << ind << "}\n";
+    }
+    for (int r = 0; r < R; ++r) {
+        os << ind << "a" << r << "_0 = f2lo(A" << r << "_0) + B" << r << "_0;\n"
+           << ind << "a" << r << "_1 = f2hi(A" << r << "_0) + f2lo(B" << r << "_1);\n"
+           << ind << "a" << r << "_2 = f2lo(A" << r << "_2) + f2hi(B" << r << "_1);\n"
+           << ind << "a" << r << "_3 = f2hi(A" << r << "_2) + f2lo(B" << r << "_3);\n"
+           << ind << "a" << r << "_4 = f2lo(A" << r << "_4) + f2hi(B" << r << "_3);\n"
+           << ind << "a" << r << "_5 = f2hi(A" << r << "_4) + f2lo(B" << r << "_5);\n"
+           << ind << "a" << r << "_6 = A" << r << "_6 + f2hi(B" << r << "_5);\n";
+    }
+}
+
 std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
                         const std::vector<int> &count) {
     std::ostringstream os;
@@ -515,19 +644,23 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
                << "{\n";
-            for (int d : ds) {
-                os << "        const float m" << d << " = ";
-                for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
-                os << ";\n";
-            }
-            for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
-                for (auto &u : uses) {
-                    const int r = u.second.first, s = u.second.second;
-                    os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
+            if (x.ffma2) {
+                emit_stencil_compute_ffma2(os, g, ds, "        ");
+            } else {
+                for (int d : ds) {
+                    os << "        const float m" << d << " = ";
+                    for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
+                    os << ";\n";
                 }
-                os << " }\n";
-            });
+                for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+                    os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                    for (auto &u : uses) {
+                        const int r = u.second.first, s = u.second.second;
+                        os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
+                    }
+                    os << " }\n";
+                });
+            }
             os << "      }\n";
         }
         // combine the tap groups in a fixed order through the staging tile:
@@ -701,16 +834,6 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     return os.str();
 }
 
-bool env_flag(const char *n) {
-    const char *v = getenv(n);
-    return v && *v && strcmp(v, "0") != 0;
-}
-
-int env_int(const char *n, int dflt) {
-    const char *v = getenv(n);
-    return (v && *v) ? atoi(v) : dflt;
-}
-
 o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH) {
     const size_t es = dtype_size(dtype);
     cuuint64_t dims[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)C, (cuuint64_t)N};
@@ -763,6 +886,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     }
     if (d.W > 256 || d.H > 256 || sp->nthreads > 1024) return false;
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
     for (const std::vector<Geo> *g : {&sp->fwd, &sp->bwd})
         if (layout_of(x, *g, true, 0).total > 220 * 1024) return false;
     if (layout_of(x, sp->fwd, false, red_bytes(x, sp->fwd)).total > 220 * 1024) return false;
