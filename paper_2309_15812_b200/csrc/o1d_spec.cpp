@@ -211,13 +211,15 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 }  // namespace
 
 struct SpecSet {
-    int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, PPC = 1, nt = 0, nsm = 0;
+    int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, PPC = 1, nt = 0, nsm = 0, gw = 1;
     std::vector<Geo> fwd, bwd;  // per distinct table
     std::vector<int> count;     // planes per table
     CUmodule mod[3] = {nullptr, nullptr, nullptr};
     CUfunction fn[3] = {nullptr, nullptr, nullptr};
+    CUfunction fin = nullptr;  // wgrad finalize
     size_t smem[3] = {0, 0, 0};
     int grid[3] = {0, 0, 0};
+    int threads[3] = {0, 0, 0};
     unsigned *d_sched = nullptr;  // 3 passes x (NT next counters + 1 done counter), then C channel counters
     std::string regs[3];
 };
@@ -244,12 +246,20 @@ __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n));
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(u64* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* b, u32 bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_expect(u64* b, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sa(b)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(u64* b, u32 ph) {
-  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n"
-               :: "r"(sa(b)), "r"(ph) : "memory");
+  // try_wait with a suspend-time hint: the warp sleeps until the phase completes
+  // instead of spinning (spin loops steal issue slots from the compute warps)
+  asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra W_%=;\n}\n"
+               :: "r"(sa(b)), "r"(ph), "r"(0x100000u) : "memory");
 }
 __device__ __forceinline__ void tma_load(void* dst, const TmaDesc* m, int x, int y, int z, int w, u64* b) {
   asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
@@ -351,6 +361,8 @@ int env_int(const char *n, int dflt) {
 struct Ctx {
     int N, C, K, Ho, Wo, BR, BC, wpg, G, PPC, nt, nsm;  // wpg: warps per tap group; G: tap groups; PPC: planes per CTA
     bool ffma2 = false;                                  // packed fp32 FMA in the stencil
+    int minb = 1;                                        // __launch_bounds__ min blocks per SM (stencil)
+    int gw = 2;                                          // tap groups of the wgrad kernel
     int nthreads() const { return 32 * wpg * G * PPC; }
     int wpp() const { return wpg * G; }  // warps per plane slot
 };
@@ -461,7 +473,10 @@ size_t tile_bytes_of(const std::vector<Geo> &geo) {
     return (b + 1023) & ~(size_t)1023;
 }
 
-size_t stage_bytes_of(const Ctx &x) { return ((size_t)x.Ho * x.Wo * 4 + 1023) & ~(size_t)1023; }
+size_t stage_bytes_of(const Ctx &x) {
+    const int rows = ((x.BR * R + 4 * R - 1) / (4 * R)) * (4 * R);  // whole 4*7-row bands
+    return ((size_t)rows * x.Wo * 4 + 1023) & ~(size_t)1023;
+}
 
 // Shared-memory layout (both kernels):
 //   tiles [2 sets][PPC] | stage [PPC] (stencil only) | wsm [2][PPC][64] | bar [2] | s_item [2][PPC] | red
@@ -575,18 +590,27 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
         for (int j : need)
             os << ind << "  const float " << vname(j) << " = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];\n";
         for (int j : pr) os << ind << "  const u64 " << pname(j) << " = f2pack(" << vname(j) << ", " << vname(j + 1) << ");\n";
-        for (auto &p : pairs) {
-            const int r = p.first, d = p.second, dw = g.taps[d].dw;
-            if (((dw % 2) + 2) % 2 == 0) {
-                for (int s = 0; s < 6; s += 2)
-                    os << ind << "  A" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
-                os << ind << "  A" << r << "_6 = fmaf(" << vname(dw + 6) << ", m" << d << ", A" << r << "_6);\n";
-            } else {
-                for (int s = 1; s < 7; s += 2)
-                    os << ind << "  B" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
-                os << ind << "  B" << r << "_0 = fmaf(" << vname(dw) << ", m" << d << ", B" << r << "_0);\n";
+        // emit slot-major (slot q of every (r, d) pair, then slot q+1, ...): consecutive
+        // instructions update different accumulators, so no FMA waits on its predecessor
+        for (int q = 0; q < 4; ++q)
+            for (auto &p : pairs) {
+                const int r = p.first, d = p.second, dw = g.taps[d].dw;
+                if (((dw % 2) + 2) % 2 == 0) {
+                    if (q < 3) {
+                        const int s = 2 * q;
+                        os << ind << "  A" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
+                    } else {
+                        os << ind << "  A" << r << "_6 = fmaf(" << vname(dw + 6) << ", m" << d << ", A" << r << "_6);\n";
+                    }
+                } else {
+                    if (q < 3) {
+                        const int s = 2 * q + 1;
+                        os << ind << "  B" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
+                    } else {
+                        os << ind << "  B" << r << "_0 = fmaf(" << vname(dw) << ", m" << d << ", B" << r << "_0);\n";
+                    }
+                }
             }
-        }
         os << ind << "}\n";
     }
     for (int r = 0; r < R; ++r) {
@@ -600,46 +624,94 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
     }
 }
 
+// Warp-specialised stencil kernel (forward / backward_input):
+//   warp 0        producer: schedules planes, stages weights, issues TMA loads
+//                 into a 2-deep ring of tiles (mbarriers full[2] / empty[2])
+//   warps 1..     consumers: 7x7 register blocks, G tap groups; after the tap
+//                 loop each warp releases the tile (empty arrive) and the
+//                 groups combine through the staging tile with pairwise named
+//                 barriers; group 0 warps TMA-store their own 4*7-row band.
+// No CTA-wide barrier in the steady state.
 std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
                         const std::vector<int> &count) {
     std::ostringstream os;
     emit_header(os, x, table_of, count);
-    const Layout L = layout_of(x, geo, true, 0);
+    const size_t TB = tile_bytes_of(geo);
+    const size_t SB = stage_bytes_of(x);
+    const size_t off_stage = 2 * TB, off_wsm = off_stage + SB, off_bar = off_wsm + 2 * 64 * 4,
+                 off_item = off_bar + 32;
+    const int ncw = x.wpg * x.G;  // consumer warps
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
-    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads() << ") o1d_stencil(const __grid_constant__ Params p) {\n"
-       << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
-    emit_thread_map(os, x);
-    emit_prologue(os, x, geo, L, true);
-    os << "  float* const stg = reinterpret_cast<float*>(smem + " << L.stage << " + pp * " << stage_bytes_of(x) << ");\n"
-       << "  float* const sto = stg + (" << R << " * br) * " << x.Wo << " + " << S << " * bc;\n"
-       << "  for (int it = 0;; ++it) {\n"
+    const int band = 4 * R;       // output rows per consumer warp
+    const int bcg = (x.BC + 7) / 8;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (ncw + 1) << ", " << x.minb
+       << ") o1d_stencil(const __grid_constant__ Params p) {\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
+       << "  float* const wsm = reinterpret_cast<float*>(smem + " << off_wsm << ");\n"
+       << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
+       << "  u64* const empty = full + 2;\n"
+       << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
+       << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  if (tid == 0) {\n"
+       << "    mbar_init(full, 32); mbar_init(full + 1, 32);\n"
+
+       << "    fence_mbar_init();\n  }\n"
+       << "  __syncthreads();\n"
+       << "  if (warp == 0) {\n"
+       << "    // ------------------------------------------------------------ producer\n"
+       << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
+       << "    for (int it = 0;; ++it) {\n"
+       << "      const int b = it & 1;\n"
+       << "      // buffer b is free once every consumer warp released item it-2: a named\n"
+       << "      // barrier per buffer parity (the producer blocks in hardware, no spinning)\n"
+       << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
+       << "      int item = -1;\n"
+       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
+       << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
+       << "      int t2 = 0, c2 = 0, n2 = 0;\n"
+       << "      if (item >= 0) item_cn(item, t2, c2, n2);\n"
+       << "      if (lane == 0 && item >= 0) {   // issue the tile load first: it is the long pole\n"
+       << "        float* dst = reinterpret_cast<float*>(smem + b * " << TB << ");\n"
+       << "        switch (t2) {\n";
+    for (int t = 0; t < x.nt; ++t)
+        os << "        case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes << "u); tma_load(dst, &p.in_map[" << t
+           << "], " << geo[t].x0 << ", " << geo[t].minDH << ", c2, n2, full + b); break;\n";
+    os << "        }\n"
+       << "      }\n"
+       << "      if (item >= 0)\n"
+       << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[b * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n"
+       << "      if (lane == 0) s_item[b] = item;\n"
+       << "      mbar_arrive(full + b);   // 32 producer arrivals (+ the tile bytes) complete the phase\n"
+       << "      if (item < 0) break;\n"
+       << "    }\n"
+       << "    if (lane == 0) sched_exit(p.sched);\n"
+       << "    return;\n"
+       << "  }\n"
+       << "  // -------------------------------------------------------------- consumers\n"
+       << "  const int cw = warp - 1, grp = cw / " << x.wpg << ", wg = cw - grp * " << x.wpg << ";\n"
+       << "  int bc = (lane & 7) + 8 * (wg % " << bcg << "), br = (lane >> 3) + 4 * (wg / " << bcg << ");\n"
+       << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
+       << "  if (!active) { bc = 0; br = 0; }\n"
+       << "  const int row0 = " << band << " * (wg / " << bcg << ");   // first output row of this warp's band\n"
+       << "  float* const stg = reinterpret_cast<float*>(smem + " << off_stage << ");\n"
+       << "  float* const sto = stg + (" << R << " * br) * " << x.Wo << " + " << S << " * bc;\n";
+    if (bcg != 1) os << "  // (several warps per band: bands are stored by the warp with wg % bcg == 0)\n";
+    os << "  for (int it = 0;; ++it) {\n"
        << "    const int b = it & 1;\n"
-       << "    if (s_item[b * PPC] < 0) break;\n"
-       << "    const int item = s_item[b * PPC + pp];\n"
-       << "    int cur[PPC];  // this set's items (s_item[b] is reused for the next set before the stores)\n"
-       << "    for (int q = 0; q < PPC; ++q) cur[q] = s_item[b * PPC + q];\n"
-       << "    int t = 0, c = 0, n = 0;\n"
-       << "    if (item >= 0) item_cn(item, t, c, n);\n"
-       << "    const float* tile = reinterpret_cast<const float*>(smem + (b * PPC + pp) * " << L.TB << ");\n"
-       << "    const float* wv = wsm + (b * PPC + pp) * 64;\n"
-       << "    mbar_wait(bar + b, (it >> 1) & 1);\n"
-       << "    if (tid == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
-       << "    if (item < 0) {\n"
-       << "      __syncthreads();\n";
-    emit_schedule(os, x, geo, L, "b", true, "      ");
-    for (int gi = x.G - 1; gi > 0; --gi) os << "      __syncthreads();\n";
-    os << "    } else switch (t) {\n";
-    auto store_pred = [&](int r, int s) {
-        std::ostringstream q;
-        if (ragged) q << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
-        return q.str();
-    };
+       << "    mbar_wait(full + b, (it >> 1) & 1);\n"
+       << "    const int item = s_item[b];\n"
+       << "    if (item < 0) break;\n"
+       << "    int t, c, n; item_cn(item, t, c, n);\n"
+       << "    const float* tile = reinterpret_cast<const float*>(smem + b * " << TB << ");\n"
+       << "    const float* wv = wsm + b * 64;\n";
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
+    os << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
-        os << "    case " << t << ": {\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "      float a" << r << "_" << s << " = 0.f;\n";
-        os << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+        os << "    case " << t << ": {\n"
+           << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < x.G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
@@ -647,6 +719,8 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
             if (x.ffma2) {
                 emit_stencil_compute_ffma2(os, g, ds, "        ");
             } else {
+                for (int r = 0; r < R; ++r)
+                    for (int s = 0; s < S; ++s) os << "        a" << r << "_" << s << " = 0.f;\n";
                 for (int d : ds) {
                     os << "        const float m" << d << " = ";
                     for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
@@ -663,70 +737,106 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
             }
             os << "      }\n";
         }
-        // combine the tap groups in a fixed order through the staging tile:
-        // y = ((acc_{G-1}) + acc_{G-2}) + ... + acc_0
-        os << "      __syncthreads();\n";
-        emit_schedule(os, x, geo, L, "b", true, "      ");
-        for (int gi = x.G - 1; gi >= 0; --gi) {
-            os << "      if (grp == " << gi << " && active) {\n";
-            for (int r = 0; r < R; ++r)
-                for (int s = 0; s < S; ++s) {
-                    os << "        " << store_pred(r, s) << "sto[" << r * x.Wo + s << "] = ";
-                    if (gi == x.G - 1)
-                        os << "a" << r << "_" << s << ";\n";
-                    else
-                        os << "sto[" << r * x.Wo + s << "] + a" << r << "_" << s << ";\n";
-                }
-            os << "      }\n";
-            if (gi > 0) os << "      __syncthreads();\n";
-        }
         os << "      break;\n    }\n";
     }
     os << "    }\n"
-       << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-       << "    __syncthreads();\n"
-       << "    if (tid == 0) {\n"
-       << "      for (int q = 0; q < PPC; ++q) {\n"
-       << "        const int itq = cur[q];\n"
-       << "        if (itq < 0) break;\n"
-       << "        int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
+       << "    __syncwarp();\n"
+       << "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");  // done with the tile\n";
+    auto store_pred = [&](int r, int s) {
+        std::ostringstream q;
+        if (ragged) q << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
+        return q.str();
+    };
+    auto emit_sts = [&](bool add) {
+        os << "      if (active) {\n";
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+                os << "        " << store_pred(r, s) << "sto[" << r * x.Wo + s << "] = ";
+                if (add) os << "sto[" << r * x.Wo + s << "] + ";
+                os << "a" << r << "_" << s << ";\n";
+            }
+        os << "      }\n";
+    };
+    // named barriers per band (warp wg of every group): id 1+wg "free" (group 0 -> others), id 1+wpg+wg chain
+    const int nb = 32 * x.G;  // threads per named barrier
+    if (x.G == 1) {
+        os << "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+           << "    __syncwarp();\n";
+        emit_sts(false);
+    } else {
+        // group G-1 writes first, then G-2 adds, ..., group 0 adds and stores.
+        os << "    if (grp == 0) {\n"
+           << "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+           << "      __syncwarp();\n"
+           << "      asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(1 + wg), \"r\"(" << nb << ") : \"memory\");\n"
+           << "    }\n";
+        for (int gi = x.G - 1; gi >= 0; --gi) {
+            os << "    if (grp == " << gi << ") {\n";
+            if (gi == x.G - 1)
+                os << "      asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + wg), \"r\"(" << nb << ") : \"memory\");\n";
+            else
+                os << "      asm volatile(\"bar.sync %0, %1;\" :: \"r\"(" << 1 + x.wpg << " + " << gi << " * " << x.wpg
+                   << " + wg), \"r\"(64) : \"memory\");\n";
+            emit_sts(gi != x.G - 1);
+            if (gi > 0)
+                os << "      asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(" << 1 + x.wpg << " + " << gi - 1 << " * "
+                   << x.wpg << " + wg), \"r\"(64) : \"memory\");\n";
+            os << "    }\n";
+        }
+    }
+    // group 0 warps store their band: rows [row0, row0 + band) of the plane
+    os << "    if (grp == 0" << (bcg != 1 ? " && (wg % " + std::to_string(bcg) + ") == 0" : std::string()) << ") {\n"
+       << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+       << "      __syncwarp();\n"
+       << "      if (lane == 0 && row0 < " << x.Ho << ") {\n"
        << "        asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
-       << "                     :: \"l\"(&p.out_map), \"r\"(sa(smem + " << L.stage << " + q * " << stage_bytes_of(x)
-       << ")), \"r\"(0), \"r\"(0), \"r\"(cq), \"r\"(nq) : \"memory\");\n"
+       << "                     :: \"l\"(&p.out_map), \"r\"(sa(stg + row0 * " << x.Wo << ")), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n) : \"memory\");\n"
+       << "        asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
        << "      }\n"
-       << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
        << "    }\n"
        << "  }\n"
-       << "  if (tid == 0) { asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\"); sched_exit(p.sched); }\n}\n";
+       << "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
+       << "}\n";
     return os.str();
 }
 
-int wgrad_rounds(const Ctx &x, const std::vector<Geo> &geo) {
-    int maxslots = 0;
-    for (auto &g : geo)
-        for (int gi = 0; gi < x.G; ++gi) maxslots = std::max(maxslots, (int)group_taps(g, gi, x.G).size());
-    return (maxslots + 31) / 32;
+size_t stencil_smem(const Ctx &x, const std::vector<Geo> &geo) {
+    return 2 * tile_bytes_of(geo) + stage_bytes_of(x) + 2 * 64 * 4 + 32 + 16;
 }
 
-size_t red_bytes(const Ctx &x, const std::vector<Geo> &geo) {
-    return 4 * 32 * wgrad_rounds(x, geo) * x.wpg * x.G * x.PPC;
-}
-
+// Warp-specialised backward_weight kernel:
+//   warp 0      producer: schedules planes, TMA-loads the x tile (per-table box,
+//               zero halo) and the dy plane (dense box) into a 2-deep ring
+//   warps 1..   consumers: GW tap groups x wpg bands; each thread keeps its 7x7
+//               block of dy in registers and accumulates one partial per
+//               distinct tap of its group; a warp reduce-scatter leaves the
+//               warp's partial of tap L in lane L; partials go to
+//               ws[plane][band][k]; the warp that completes a channel (epoch
+//               counter) sums them in f64 in (n, band) order into dW.
 std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
                       const std::vector<int> &count) {
     std::ostringstream os;
     emit_header(os, x, table_of, count);
-    const Layout L = layout_of(x, geo, false, red_bytes(x, geo));
-    const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
-    const int rounds = wgrad_rounds(x, geo);
+    const int G = x.G;
+    const size_t TB = tile_bytes_of(geo);
+    const int dyp = (S * x.BC + 3) & ~3;     // dy box pitch: whole 7-col blocks, 16-byte rows (zero-filled past Wo)
+    const int dyrows = R * x.BR;             // padded rows, zero-filled by TMA
+    const size_t DB = ((size_t)dyp * dyrows * 4 + 1023) & ~(size_t)1023;
+    const int ncw = x.wpg * G;
+    const size_t off_dy = 2 * TB, off_scr = off_dy + 2 * DB, off_bar = off_scr + (size_t)ncw * 32 * 4,
+                 off_item = off_bar + 32;
+    int maxd = 0;
     std::vector<std::vector<int>> k2g(x.nt, std::vector<int>(x.K)), k2s(x.nt, std::vector<int>(x.K));
     for (int t = 0; t < x.nt; ++t)
-        for (int gi = 0; gi < x.G; ++gi) {
-            const std::vector<int> ds = group_taps(geo[t], gi, x.G);
+        for (int gi = 0; gi < G; ++gi) {
+            const std::vector<int> ds = group_taps(geo[t], gi, G);
+            maxd = std::max(maxd, (int)ds.size());
             for (int k = 0; k < x.K; ++k)
                 for (size_t q = 0; q < ds.size(); ++q)
                     if (geo[t].k2d[k] == ds[q]) k2g[t][k] = gi, k2s[t][k] = (int)q;
         }
+    int NV = 1;
+    while (NV < maxd) NV *= 2;  // reduce-scatter width (<= 32: K <= 64 and G >= 2, or K <= 32)
     os << "__constant__ unsigned char K2G[" << x.nt << "][" << x.K << "] = {";
     for (int t = 0; t < x.nt; ++t) {
         os << (t ? "," : "") << "{";
@@ -740,98 +850,128 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
         os << "}";
     }
     os << "};\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(" << x.nthreads() << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
-       << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
-    emit_thread_map(os, x);
-    emit_prologue(os, x, geo, L, false);
-    os << "  float* red = reinterpret_cast<float*>(smem + " << L.red << ");\n"
-       << "  const float* const dyp = reinterpret_cast<const float*>(p.io);\n";
-    auto emit_dy_load = [&](const char *dst, const char *itemexpr) {
-        os << "    {\n      const int itm = " << itemexpr << ";\n"
-           << "      if (itm >= 0 && active) {\n        int tt, cc, nn; item_cn(itm, tt, cc, nn);\n"
-           << "        const float* gp = dyp + ((u64)(nn * " << x.C << " + cc) * " << x.Ho << " + " << R << " * br) * "
-           << x.Wo << " + " << S << " * bc;\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) {
-                os << "        " << dst << r << "_" << s << " = ";
-                if (ragged)
-                    os << "(" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < "
-                       << x.Wo << ") ? __ldg(gp + " << r * x.Wo + s << ") : 0.f;\n";
-                else
-                    os << "__ldg(gp + " << r * x.Wo + s << ");\n";
-            }
-        os << "      } else {\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "        " << dst << r << "_" << s << " = 0.f;\n";
-        os << "      }\n    }\n";
-    };
-    for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s) os << "  float g" << r << "_" << s << ", h" << r << "_" << s << ";\n";
-    emit_dy_load("g", "s_item[pp]");
-    os << "  float v0[32]";
-    for (int rd = 1; rd < rounds; ++rd) os << ", v" << rd << "[32]";
-    os << ";\n  for (int it = 0;; ++it) {\n"
+    // reduce-scatter of NV values over the warp: lane L ends with the warp sum of v[L % NV]
+    os << "__device__ __forceinline__ float reduce_scatter_nv(float (&v)[" << NV << "], int lane) {\n"
+       << "#pragma unroll\n"
+       << "  for (int s = " << NV / 2 << "; s >= 1; s >>= 1) {\n"
+       << "    const bool up = lane & s;\n"
+       << "#pragma unroll\n"
+       << "    for (int i = 0; i < s; ++i) {\n"
+       << "      const float send = up ? v[i] : v[i + s];\n"
+       << "      const float keep = up ? v[i + s] : v[i];\n"
+       << "      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);\n"
+       << "    }\n  }\n"
+       << "  float r = v[0];\n"
+       << "#pragma unroll\n"
+       << "  for (int s = " << NV << "; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);\n"
+       << "  return r;\n}\n";
+    const int bcg = (x.BC + 7) / 8;
+    const unsigned target = (unsigned)(x.N * ncw);
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (ncw + 1) << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
+       << "  float* const scr = reinterpret_cast<float*>(smem + " << off_scr << ");\n"
+       << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
+       << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
+       << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  if (tid == 0) { mbar_init(full, 32); mbar_init(full + 1, 32); fence_mbar_init(); }\n"
+       << "  __syncthreads();\n"
+       << "  if (warp == 0) {\n"
+       << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
+       << "    for (int it = 0;; ++it) {\n"
+       << "      const int b = it & 1;\n"
+       << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
+       << "      int item = -1;\n"
+       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
+       << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
+       << "      if (lane == 0) {\n"
+       << "        s_item[b] = item;\n"
+       << "        if (item >= 0) {\n"
+       << "          int t2, c2, n2; item_cn(item, t2, c2, n2);\n"
+       << "          float* dst = reinterpret_cast<float*>(smem + b * " << TB << ");\n"
+       << "          switch (t2) {\n";
+    for (int t = 0; t < x.nt; ++t)
+        os << "          case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes + (uint32_t)(dyp * dyrows * 4)
+           << "u); tma_load(dst, &p.in_map[" << t << "], " << geo[t].x0 << ", " << geo[t].minDH
+           << ", c2, n2, full + b); break;\n";
+    os << "          }\n"
+       << "          tma_load(smem + " << off_dy << " + b * " << DB << ", &p.out_map, 0, 0, c2, n2, full + b);\n"
+       << "        }\n"
+       << "      }\n"
+       << "      mbar_arrive(full + b);\n"
+       << "      if (item < 0) break;\n"
+       << "    }\n"
+       << "    if (lane == 0) sched_exit(p.sched);\n"
+       << "    return;\n"
+       << "  }\n"
+       << "  const int cw = warp - 1, grp = cw / " << x.wpg << ", wg = cw - grp * " << x.wpg << ";\n"
+       << "  int bc = (lane & 7) + 8 * (wg % " << bcg << "), br = (lane >> 3) + 4 * (wg / " << bcg << ");\n"
+       << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
+       << "  if (!active) { bc = 0; br = 0; }\n"
+       << "  float v[" << NV << "];\n"
+       << "  for (int it = 0;; ++it) {\n"
        << "    const int b = it & 1;\n"
-       << "    if (s_item[b * PPC] < 0) break;\n"
-       << "    const int item = s_item[b * PPC + pp];\n"
-       << "    int t = 0, c = 0, n = 0;\n"
-       << "    if (item >= 0) item_cn(item, t, c, n);\n";
-    emit_dy_load("h", "s_item[(b ^ 1) * PPC + pp]");  // prefetch the next set's dy (its tiles are in flight)
-    os << "    const float* tile = reinterpret_cast<const float*>(smem + (b * PPC + pp) * " << L.TB << ");\n"
-       << "    mbar_wait(bar + b, (it >> 1) & 1);\n";
-    for (int rd = 0; rd < rounds; ++rd)
-        os << "    for (int q = 0; q < 32; ++q) v" << rd << "[q] = 0.f;\n";
-    os << "    if (item >= 0) switch (t) {\n";
+       << "    mbar_wait(full + b, (it >> 1) & 1);\n"
+       << "    const int item = s_item[b];\n"
+       << "    if (item < 0) break;\n"
+       << "    int t, c, n; item_cn(item, t, c, n);\n"
+       << "    const float* tile = reinterpret_cast<const float*>(smem + b * " << TB << ");\n"
+       << "    const float* gb = reinterpret_cast<const float*>(smem + " << off_dy << " + b * " << DB << ") + (" << R
+       << " * br) * " << dyp << " + " << S << " * bc;\n";
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s)
+            os << "    const float g" << r << "_" << s << " = active ? gb[" << r * dyp + s << "] : 0.f;\n";
+    os << "    for (int q = 0; q < " << NV << "; ++q) v[q] = 0.f;\n"
+       << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
            << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
-        for (int gi = 0; gi < x.G; ++gi) {
-            const std::vector<int> ds = group_taps(g, gi, x.G);
-            os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
-               << "{\n";
+        for (int gi = 0; gi < G; ++gi) {
+            const std::vector<int> ds = group_taps(g, gi, G);
+            os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
             for (int d : ds) os << "        float q" << d << " = 0.f;\n";
             for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                os << "        { const float px = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
                 for (auto &u : uses)
-                    os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", v, q"
+                    os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q"
                        << u.first << ");";
                 os << " }\n";
             });
-            for (size_t q = 0; q < ds.size(); ++q) os << "        v" << q / 32 << "[" << q % 32 << "] = q" << ds[q] << ";\n";
+            for (size_t q = 0; q < ds.size(); ++q) os << "        v[" << q << "] = q" << ds[q] << ";\n";
             os << "      }\n";
         }
         os << "      break;\n    }\n";
     }
-    os << "    }\n";
-    for (int rd = 0; rd < rounds; ++rd)
-        os << "    red[warp * " << 32 * rounds << " + " << 32 * rd << " + lane] = reduce_scatter32(v" << rd
-           << ", lane);\n";
-    os << "    __syncthreads();\n";
-    emit_schedule(os, x, geo, L, "b", false, "    ");
-    os << "    if (item >= 0) {\n"
-       << "      float* wsp = p.ws + (u64)(c * " << x.N << " + n) * " << x.K << ";\n"
-       << "      for (int k = ptid; k < " << x.K << "; k += " << 32 * x.wpp() << ") {\n"
-       << "        const float* rp = red + ((pp * " << x.G << " + K2G[t][k]) * " << x.wpg << ") * " << 32 * rounds
-       << " + K2S[t][k];\n"
-       << "        float s = 0.f;\n"
-       << "        for (int w = 0; w < " << x.wpg << "; ++w) s += rp[w * " << 32 * rounds << "];\n"
-       << "        wsp[k] = s;\n      }\n"
-       << "      __threadfence();\n    }\n"
-       << "    __syncthreads();\n"
-       << "    if (item >= 0 && warp == pp * " << x.wpp() << ") {\n      unsigned last = 0;\n"
-       << "      if (lane == 0) last = ((atomicAdd(p.cnt + c, 1u) + 1u) % " << x.N << "u) == 0u;\n"
-       << "      last = __shfl_sync(0xffffffffu, last, 0);\n"
-       << "      if (last) {\n        __threadfence();\n"
-       << "        for (int k = lane; k < " << x.K << "; k += 32) {\n          double s = 0.0;\n"
-       << "          const float* col = p.ws + (u64)c * " << x.N << " * " << x.K << " + k;\n"
+    os << "    }\n"
+       << "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");  // tile + dy released\n"
+       << "    const float part = reduce_scatter_nv(v, lane);\n"
+       << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
+       << "    __syncwarp();\n"
+       << "    float* wsp = p.ws + ((u64)(c * " << x.N << " + n) * " << x.wpg << " + wg) * " << x.K << ";\n"
+       << "    for (int k = lane; k < " << x.K << "; k += 32)\n"
+       << "      if (K2G[t][k] == grp) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
+       << "  }\n"
+       << "}\n";
+    // finalize (second launch; the kernel boundary orders the partial writes):
+    // dW[c][k] = sum over (n, band) of the partials, f64, fixed order
+    os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
+       << "  const int i = blockIdx.x * blockDim.x + threadIdx.x;\n"
+       << "  if (i >= " << x.C * x.K << ") return;\n"
+       << "  const int c = i / " << x.K << ", k = i - c * " << x.K << ";\n"
+       << "  const float* col = ws + (u64)c * " << x.N * x.wpg << " * " << x.K << " + k;\n"
+       << "  double s = 0.0;\n"
        << "#pragma unroll 8\n"
-       << "          for (int i = 0; i < " << x.N << "; ++i) s += (double)__ldcg(col + (u64)i * " << x.K << ");\n"
-       << "          p.dW[c * " << x.K << " + k] = (float)s;\n        }\n      }\n    }\n";
-    for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s) os << "    g" << r << "_" << s << " = h" << r << "_" << s << ";\n";
-    os << "  }\n  if (tid == 0) sched_exit(p.sched);\n}\n";
+       << "  for (int j = 0; j < " << x.N * x.wpg << "; ++j) s += (double)col[(u64)j * " << x.K << "];\n"
+       << "  dW[i] = (float)s;\n"
+       << "}\n";
     return os.str();
+}
+
+size_t wgrad_smem(const Ctx &x, const std::vector<Geo> &geo) {
+    const size_t TB = tile_bytes_of(geo);
+    const size_t DB = ((size_t)((S * x.BC + 3) & ~3) * R * x.BR * 4 + 1023) & ~(size_t)1023;
+    return 2 * TB + 2 * DB + (size_t)x.wpg * x.G * 32 * 4 + 32 + 16;
 }
 
 o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH) {
@@ -885,15 +1025,28 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
             if (g->pitch > 256 || g->rows > 256 || g->bytes > 100 * 1024) return false;
     }
     if (d.W > 256 || d.H > 256 || sp->nthreads > 1024) return false;
+    if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
+    x.minb = env_int("O1D_MINB", 3);
+    x.gw = env_int("O1D_GW", 2);
+    if (x.gw < 1 || x.gw > 8) return false;
+    {
+        int maxd = 0;
+        for (auto &g : sp->fwd)
+            for (int gi = 0; gi < x.gw; ++gi) maxd = std::max(maxd, (int)group_taps(g, gi, x.gw).size());
+        if (maxd > 32) return false;
+    }
+    Ctx xw = x;
+    xw.G = x.gw;
     for (const std::vector<Geo> *g : {&sp->fwd, &sp->bwd})
-        if (layout_of(x, *g, true, 0).total > 220 * 1024) return false;
-    if (layout_of(x, sp->fwd, false, red_bytes(x, sp->fwd)).total > 220 * 1024) return false;
+        if (stencil_smem(x, *g) > 220 * 1024) return false;
+    if (wgrad_smem(xw, sp->fwd) > 220 * 1024) return false;
     std::vector<int> table_of(pl->table_of.begin(), pl->table_of.end());
     src[0] = gen_stencil(x, sp->fwd, table_of, sp->count);
     src[1] = gen_stencil(x, sp->bwd, table_of, sp->count);
-    src[2] = gen_wgrad(x, sp->fwd, table_of, sp->count);
+    src[2] = gen_wgrad(xw, sp->fwd, table_of, sp->count);
+    sp->gw = x.gw;
     return true;
 }
 
@@ -936,9 +1089,13 @@ o1d_status spec_create(o1d_plan *pl) {
             return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
         }
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
-    sp->smem[0] = layout_of(x, sp->fwd, true, 0).total;
-    sp->smem[1] = layout_of(x, sp->bwd, true, 0).total;
-    sp->smem[2] = layout_of(x, sp->fwd, false, red_bytes(x, sp->fwd)).total;
+    sp->smem[0] = stencil_smem(x, sp->fwd);
+    sp->smem[1] = stencil_smem(x, sp->bwd);
+    sp->threads[0] = sp->threads[1] = 32 * (sp->wpg * sp->G + 1);
+    Ctx xw = x;
+    xw.G = sp->gw;
+    sp->threads[2] = 32 * (sp->wpg * sp->gw + 1);
+    sp->smem[2] = wgrad_smem(xw, sp->fwd);
     const char *fnames[3] = {"o1d_stencil", "o1d_stencil", "o1d_wgrad"};
     PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occ = nullptr;
     std::string e;
@@ -947,10 +1104,11 @@ o1d_status spec_create(o1d_plan *pl) {
     for (int i = 0; i < 3; ++i) {
         CUresult r = dr.moduleLoadData(&sp->mod[i], cubin[i].data());
         if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&sp->fn[i], sp->mod[i], fnames[i]);
+        if (r == CUDA_SUCCESS && i == 2) r = dr.moduleGetFunction(&sp->fin, sp->mod[i], "o1d_wgrad_finalize");
         if (r == CUDA_SUCCESS)
             r = dr.funcSetAttribute(sp->fn[i], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)sp->smem[i]);
         int blocks = 0;
-        if (r == CUDA_SUCCESS && occ) r = occ(&blocks, sp->fn[i], sp->nthreads, sp->smem[i]);
+        if (r == CUDA_SUCCESS && occ) r = occ(&blocks, sp->fn[i], sp->threads[i], sp->smem[i]);
         if (r != CUDA_SUCCESS || blocks < 1) {
             for (int j = 0; j <= i; ++j)
                 if (sp->mod[j]) dr.moduleUnload(sp->mod[j]);
@@ -993,10 +1151,10 @@ void spec_destroy(o1d_plan *pl) {
 }
 
 bool spec_has(const o1d_plan *pl, int pass) { return pl->spec && pass >= 0 && pass < 3; }
-int spec_launches(const o1d_plan *, int) { return 1; }
+int spec_launches(const o1d_plan *, int pass) { return pass == 2 ? 2 : 1; }
 size_t spec_workspace_bytes(const o1d_plan *pl) {
     if (!pl->spec) return 0;
-    return sizeof(float) * (size_t)pl->d.N * pl->d.C * pl->d.K;
+    return sizeof(float) * (size_t)pl->d.N * pl->d.C * pl->spec->wpg * pl->d.K;
 }
 
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW, float *ws,
@@ -1011,11 +1169,12 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
     for (int t = 0; t < nt; ++t)
         if (o1d_status st = encode(&maps[t], a, d.dtype, inW, inH, d.C, d.N, geo[t].pitch, geo[t].rows)) return st;
-    if (pass != 2) {  // dense output box for the TMA store
+    if (pass != 2) {  // dense output band box for the TMA store
         const int oW = pass == 1 ? d.W : pl->Q, oH = pass == 1 ? d.H : pl->P;
-        if (o1d_status st = encode(&maps[nt], b, d.dtype, oW, oH, d.C, d.N, oW, oH)) return st;
-    } else {
-        memset(&maps[nt], 0, sizeof(CUtensorMap));
+        if (o1d_status st = encode(&maps[nt], b, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
+    } else {  // dy plane, rows padded to whole 7-row blocks (zero-filled)
+        if (o1d_status st = encode(&maps[nt], b, d.dtype, pl->Q, pl->P, d.C, d.N, (S * sp->BC + 3) & ~3, R * sp->BR))
+            return st;
     }
     void **ptrs = reinterpret_cast<void **>(blob + sizeof(CUtensorMap) * (nt + 1));
     ptrs[0] = const_cast<float *>(w);
@@ -1025,9 +1184,16 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[4] = sp->d_sched + 3 * (nt + 1);
     ptrs[5] = dW;
     void *args[] = {blob};
-    CUresult r = drv().launchKernel(sp->fn[pass], (unsigned)sp->grid[pass], 1, 1, sp->nthreads, 1, 1,
+    CUresult r = drv().launchKernel(sp->fn[pass], (unsigned)sp->grid[pass], 1, 1, sp->threads[pass], 1, 1,
                                     (unsigned)sp->smem[pass], static_cast<CUstream>(stream), args, nullptr);
     if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of specialised kernel: " + cu_err(r));
+    if (pass == 2) {
+        const void *wsp = ws;
+        void *fargs[] = {&wsp, &dW};
+        const unsigned n = (unsigned)(d.C * d.K);
+        r = drv().launchKernel(sp->fin, (n + 255) / 256, 1, 1, 256, 1, 1, 0, static_cast<CUstream>(stream), fargs, nullptr);
+        if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of wgrad finalize: " + cu_err(r));
+    }
     return O1D_OK;
 }
 
