@@ -363,12 +363,25 @@ struct Ctx {
     bool ffma2 = false;                                  // packed fp32 FMA in the stencil
     int minb = 1;                                        // __launch_bounds__ min blocks per SM (stencil)
     int gw = 2;                                          // tap groups of the wgrad kernel
+    int act = 0;                                         // activation dtype (o1d_dtype)
     int nthreads() const { return 32 * wpg * G * PPC; }
     int wpp() const { return wpg * G; }  // warps per plane slot
 };
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
     os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define PPC " << x.PPC << "\n";
+    // activation element type in shared memory / HBM; arithmetic is fp32 throughout
+    if (x.act == O1D_F32)
+        os << "typedef float act_t;\n#define LD(v) (v)\n"
+              "__device__ __forceinline__ float to_act(float v) { return v; }\n";
+    else if (x.act == O1D_BF16)
+        os << "typedef unsigned short act_t;\n#define LD(v) __uint_as_float(((unsigned)(v)) << 16)\n"
+              "__device__ __forceinline__ act_t to_act(float v) { unsigned short r; asm(\"cvt.rn.bf16.f32 %0, %1;\" : \"=h\"(r) : \"f\"(v)); return r; }\n";
+    else
+        os << "typedef unsigned short act_t;\n"
+              "__device__ __forceinline__ float h2f(unsigned short h) { float f; asm(\"cvt.f32.f16 %0, %1;\" : \"=f\"(f) : \"h\"(h)); return f; }\n"
+              "#define LD(v) h2f(v)\n"
+              "__device__ __forceinline__ act_t to_act(float v) { unsigned short r; asm(\"cvt.rn.f16.f32 %0, %1;\" : \"=h\"(r) : \"f\"(v)); return r; }\n";
     {
         long tot = 0;
         for (int t = 0; t < x.nt; ++t) tot += count[t];
@@ -588,7 +601,7 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
         for (int j : pr) need.insert(j), need.insert(j + 1);
         os << ind << "{\n";
         for (int j : need)
-            os << ind << "  const float " << vname(j) << " = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];\n";
+            os << ind << "  const float " << vname(j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
         for (int j : pr) os << ind << "  const u64 " << pname(j) << " = f2pack(" << vname(j) << ", " << vname(j + 1) << ");\n";
         // emit slot-major (slot q of every (r, d) pair, then slot q+1, ...): consecutive
         // instructions update different accumulators, so no FMA waits on its predecessor
@@ -703,7 +716,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const float* tile = reinterpret_cast<const float*>(smem + b * " << TB << ");\n"
+       << "    const act_t* tile = reinterpret_cast<const act_t*>(smem + b * " << TB << ");\n"
        << "    const float* wv = wsm + b * 64;\n";
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
@@ -711,7 +724,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const act_t* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < x.G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
@@ -727,7 +740,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
                     os << ";\n";
                 }
                 for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                    os << "        { const float v = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                    os << "        { const float v = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
                     for (auto &u : uses) {
                         const int r = u.second.first, s = u.second.second;
                         os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
@@ -747,14 +760,36 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
         if (ragged) q << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
         return q.str();
     };
-    auto emit_sts = [&](bool add) {
-        os << "      if (active) {\n";
+    // partial (fp32) or final write of the block into the band's staging area;
+    // final 16-bit outputs are packed in place (pitch Wo) once the warp has read
+    // its fp32 partials, so the TMA store reads a dense act_t band
+    auto emit_sts = [&](bool add, bool final_) {
+        if (!final_ || x.act == O1D_F32) {
+            os << "      if (active) {\n";
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) {
+                    os << "        " << store_pred(r, s) << "sto[" << r * x.Wo + s << "] = ";
+                    if (add) os << "sto[" << r * x.Wo + s << "] + ";
+                    os << "a" << r << "_" << s << ";\n";
+                }
+            os << "      }\n";
+            return;
+        }
+        if (add) {
+            os << "      if (active) {\n";
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s)
+                    os << "        " << store_pred(r, s) << "a" << r << "_" << s << " = sto[" << r * x.Wo + s << "] + a"
+                       << r << "_" << s << ";\n";
+            os << "      }\n";
+        }
+        os << "      __syncwarp();\n"
+           << "      if (active) {\n"
+           << "        act_t* stb = reinterpret_cast<act_t*>(stg + row0 * " << x.Wo << ") + (" << R << " * br - row0) * "
+           << x.Wo << " + " << S << " * bc;\n";
         for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) {
-                os << "        " << store_pred(r, s) << "sto[" << r * x.Wo + s << "] = ";
-                if (add) os << "sto[" << r * x.Wo + s << "] + ";
-                os << "a" << r << "_" << s << ";\n";
-            }
+            for (int s = 0; s < S; ++s)
+                os << "        " << store_pred(r, s) << "stb[" << r * x.Wo + s << "] = to_act(a" << r << "_" << s << ");\n";
         os << "      }\n";
     };
     // named barriers per band (warp wg of every group): id 1+wg "free" (group 0 -> others), id 1+wpg+wg chain
@@ -762,7 +797,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     if (x.G == 1) {
         os << "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
            << "    __syncwarp();\n";
-        emit_sts(false);
+        emit_sts(false, true);
     } else {
         // group G-1 writes first, then G-2 adds, ..., group 0 adds and stores.
         os << "    if (grp == 0) {\n"
@@ -777,7 +812,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
             else
                 os << "      asm volatile(\"bar.sync %0, %1;\" :: \"r\"(" << 1 + x.wpg << " + " << gi << " * " << x.wpg
                    << " + wg), \"r\"(64) : \"memory\");\n";
-            emit_sts(gi != x.G - 1);
+            emit_sts(gi != x.G - 1, gi == 0);
             if (gi > 0)
                 os << "      asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(" << 1 + x.wpg << " + " << gi - 1 << " * "
                    << x.wpg << " + wg), \"r\"(64) : \"memory\");\n";
@@ -819,9 +854,10 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     emit_header(os, x, table_of, count);
     const int G = x.G;
     const size_t TB = tile_bytes_of(geo);
-    const int dyp = (S * x.BC + 3) & ~3;     // dy box pitch: whole 7-col blocks, 16-byte rows (zero-filled past Wo)
+    const int es = x.act == O1D_F32 ? 4 : 2, vec = 16 / es;
+    const int dyp = (S * x.BC + vec - 1) & ~(vec - 1);  // dy box pitch: whole 7-col blocks, 16-byte rows (zero-filled past Wo)
     const int dyrows = R * x.BR;             // padded rows, zero-filled by TMA
-    const size_t DB = ((size_t)dyp * dyrows * 4 + 1023) & ~(size_t)1023;
+    const size_t DB = ((size_t)dyp * dyrows * es + 1023) & ~(size_t)1023;
     const int ncw = x.wpg * G;
     const size_t off_dy = 2 * TB, off_scr = off_dy + 2 * DB, off_bar = off_scr + (size_t)ncw * 32 * 4,
                  off_item = off_bar + 32;
@@ -891,7 +927,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "          float* dst = reinterpret_cast<float*>(smem + b * " << TB << ");\n"
        << "          switch (t2) {\n";
     for (int t = 0; t < x.nt; ++t)
-        os << "          case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes + (uint32_t)(dyp * dyrows * 4)
+        os << "          case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes + (uint32_t)(dyp * dyrows * es)
            << "u); tma_load(dst, &p.in_map[" << t << "], " << geo[t].x0 << ", " << geo[t].minDH
            << ", c2, n2, full + b); break;\n";
     os << "          }\n"
@@ -915,24 +951,24 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const float* tile = reinterpret_cast<const float*>(smem + b * " << TB << ");\n"
-       << "    const float* gb = reinterpret_cast<const float*>(smem + " << off_dy << " + b * " << DB << ") + (" << R
+       << "    const act_t* tile = reinterpret_cast<const act_t*>(smem + b * " << TB << ");\n"
+       << "    const act_t* gb = reinterpret_cast<const act_t*>(smem + " << off_dy << " + b * " << DB << ") + (" << R
        << " * br) * " << dyp << " + " << S << " * bc;\n";
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s)
-            os << "    const float g" << r << "_" << s << " = active ? gb[" << r * dyp + s << "] : 0.f;\n";
+            os << "    const float g" << r << "_" << s << " = active ? LD(gb[" << r * dyp + s << "]) : 0.f;\n";
     os << "    for (int q = 0; q < " << NV << "; ++q) v[q] = 0.f;\n"
        << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const float* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const act_t* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
             for (int d : ds) os << "        float q" << d << " = 0.f;\n";
             for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                os << "        { const float px = tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "];";
+                os << "        { const float px = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
                 for (auto &u : uses)
                     os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q"
                        << u.first << ");";
@@ -970,7 +1006,8 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
 
 size_t wgrad_smem(const Ctx &x, const std::vector<Geo> &geo) {
     const size_t TB = tile_bytes_of(geo);
-    const size_t DB = ((size_t)((S * x.BC + 3) & ~3) * R * x.BR * 4 + 1023) & ~(size_t)1023;
+    const int es = x.act == O1D_F32 ? 4 : 2, vec = 16 / es;
+    const size_t DB = ((size_t)((S * x.BC + vec - 1) & ~(vec - 1)) * R * x.BR * es + 1023) & ~(size_t)1023;
     return 2 * TB + 2 * DB + (size_t)x.wpg * x.G * 32 * 4 + 32 + 16;
 }
 
@@ -998,8 +1035,9 @@ o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int 
 // Returns false (and no sources) when the plan is not eligible.
 bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) {
     const o1d_desc &d = pl->d;
-    if (d.stride != 1 || d.dtype != O1D_F32) return false;
-    if ((d.W * 4) % 16 != 0 || d.K > 64) return false;
+    const int es = (int)dtype_size(d.dtype);
+    if (d.stride != 1) return false;
+    if ((d.W * es) % 16 != 0 || d.K > 64) return false;
     if (pl->n_distinct > 16 || (long)d.N * d.C >= (1L << 22)) return false;
     sp->BR = (pl->P + R - 1) / R;
     sp->BC = (pl->Q + S - 1) / S;
@@ -1019,8 +1057,8 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     }
     for (int t = 0; t < sp->nt; ++t) {
         const int c = rep[t];
-        sp->fwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, false, sp->BR, sp->BC, 4));
-        sp->bwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, true, sp->BR, sp->BC, 4));
+        sp->fwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, false, sp->BR, sp->BC, es));
+        sp->bwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, true, sp->BR, sp->BC, es));
         for (const Geo *g : {&sp->fwd.back(), &sp->bwd.back()})
             if (g->pitch > 256 || g->rows > 256 || g->bytes > 100 * 1024) return false;
     }
@@ -1028,6 +1066,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
+    x.act = d.dtype;
     x.minb = env_int("O1D_MINB", 3);
     x.gw = env_int("O1D_GW", 2);
     if (x.gw < 1 || x.gw > 8) return false;
@@ -1089,6 +1128,7 @@ o1d_status spec_create(o1d_plan *pl) {
             return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
         }
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    x.act = d.dtype;
     sp->smem[0] = stencil_smem(x, sp->fwd);
     sp->smem[1] = stencil_smem(x, sp->bwd);
     sp->threads[0] = sp->threads[1] = 32 * (sp->wpg * sp->G + 1);
@@ -1173,7 +1213,8 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
         const int oW = pass == 1 ? d.W : pl->Q, oH = pass == 1 ? d.H : pl->P;
         if (o1d_status st = encode(&maps[nt], b, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
     } else {  // dy plane, rows padded to whole 7-row blocks (zero-filled)
-        if (o1d_status st = encode(&maps[nt], b, d.dtype, pl->Q, pl->P, d.C, d.N, (S * sp->BC + 3) & ~3, R * sp->BR))
+        const int vec = 16 / (int)dtype_size(d.dtype);
+        if (o1d_status st = encode(&maps[nt], b, d.dtype, pl->Q, pl->P, d.C, d.N, (S * sp->BC + vec - 1) & ~(vec - 1), R * sp->BR))
             return st;
     }
     void **ptrs = reinterpret_cast<void **>(blob + sizeof(CUtensorMap) * (nt + 1));
