@@ -184,7 +184,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2309_15812_b200 import binding as B
-    from paper_2309_15812_b200 import inputs
+    from paper_2309_15812_b200 import dp, inputs
 
     world, rank, local = dist_env()
     if world > 1:
@@ -226,7 +226,7 @@ def run_ours(args):
         if ev is not None:
             ev[3].record(stream)
         if world > 1:
-            dist.all_reduce(dW)  # row a8: NCCL sum of the weight gradient over NVLink
+            dp.allreduce_weight_grad(dW)  # row a8: NCCL sum of the weight gradient over NVLink
 
     for i in range(args.warmup):
         step(i)
