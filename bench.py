@@ -35,7 +35,7 @@ PASSES = ("forward", "backward_input", "backward_weight")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -137,7 +137,7 @@ def cpu_baseline(wl, dtype_name, target_s=12.0):
     th = max(1, oracle.max_threads())
     angles = T.direction_angles(wl.D, wl.C, wl.assign)
     oh, ow = (np.array(a, np.int32) for a in T.taps_table(wl.K, wl.pad, angles))
-    n = max(1, wl.N // 8)
+    n = wl.N
     x = inputs.activation((n, wl.C, wl.H, wl.W), 0, dtype_name).astype(np.float64)
     dy = inputs.activation((n, wl.C, wl.H, wl.W), 2, dtype_name).astype(np.float64)
     w = inputs.weights(wl.C, wl.K, 1).astype(np.float64)
@@ -149,7 +149,7 @@ def cpu_baseline(wl, dtype_name, target_s=12.0):
         oracle.backward_weight(x, dy, oh, ow, 1, th)
         steps += 1
         el = time.perf_counter() - t0
-        if el >= target_s or steps >= 200:
+        if el >= target_s or steps >= 100000:
             break
     es = 4 if dtype_name == "f32" else 2
     from dataclasses import replace

@@ -991,15 +991,25 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "}\n";
     // finalize (second launch; the kernel boundary orders the partial writes):
     // dW[c][k] = sum over (n, band) of the partials, f64, fixed order
+    // One CTA per channel: thread (j, k) sums entries j, j+8, ... of column k
+    // (all loads in flight), then a fixed-order f64 sum over j.
+    const int NE = x.N * x.wpg;
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
-       << "  const int i = blockIdx.x * blockDim.x + threadIdx.x;\n"
-       << "  if (i >= " << x.C * x.K << ") return;\n"
-       << "  const int c = i / " << x.K << ", k = i - c * " << x.K << ";\n"
-       << "  const float* col = ws + (u64)c * " << x.N * x.wpg << " * " << x.K << " + k;\n"
-       << "  double s = 0.0;\n"
-       << "#pragma unroll 8\n"
-       << "  for (int j = 0; j < " << x.N * x.wpg << "; ++j) s += (double)col[(u64)j * " << x.K << "];\n"
-       << "  dW[i] = (float)s;\n"
+       << "  __shared__ double part[8][64];\n"
+       << "  const int c = blockIdx.x, j = threadIdx.x >> 5 /* 0..7 */, lane = threadIdx.x & 31;\n"
+       << "  const float* base = ws + (u64)c * " << NE << " * " << x.K << ";\n"
+       << "  for (int k = lane; k < " << x.K << "; k += 32) {\n"
+       << "    double s = 0.0;\n"
+       << "#pragma unroll 16\n"
+       << "    for (int e = j; e < " << NE << "; e += 8) s += (double)__ldcg(base + (u64)e * " << x.K << " + k);\n"
+       << "    part[j][k] = s;\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  if (threadIdx.x < " << x.K << ") {\n"
+       << "    double s = 0.0;\n"
+       << "    for (int q = 0; q < 8; ++q) s += part[q][threadIdx.x];\n"
+       << "    dW[c * " << x.K << " + threadIdx.x] = (float)s;\n"
+       << "  }\n"
        << "}\n";
     return os.str();
 }
@@ -1158,7 +1168,9 @@ o1d_status spec_create(o1d_plan *pl) {
         }
         sp->grid[i] = (int)std::min<long>(planes, (long)blocks * nsm);
         const std::string &lg = logs[i];
-        size_t pos = lg.find("Used ");
+        size_t fpos = lg.find(std::string("for ") + fnames[i] + "\n");
+        if (fpos == std::string::npos) fpos = lg.find(std::string("Compiling entry function '") + fnames[i] + "'");
+        size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
         sp->regs[i] = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
     }
     const size_t nsched = 3 * (sp->nt + 1) + d.C;
@@ -1231,8 +1243,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     if (pass == 2) {
         const void *wsp = ws;
         void *fargs[] = {&wsp, &dW};
-        const unsigned n = (unsigned)(d.C * d.K);
-        r = drv().launchKernel(sp->fin, (n + 255) / 256, 1, 1, 256, 1, 1, 0, static_cast<CUstream>(stream), fargs, nullptr);
+        r = drv().launchKernel(sp->fin, (unsigned)d.C, 1, 1, 256, 1, 1, 0, static_cast<CUstream>(stream), fargs, nullptr);
         if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of wgrad finalize: " + cu_err(r));
     }
     return O1D_OK;
