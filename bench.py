@@ -126,6 +126,16 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(pass_name):
+    """DRAM bytes per launch of `pass_name` from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            v = json.load(f).get(pass_name)
+        return float(v) if v is not None else None
+    except Exception:
+        return None
+
+
 def cpu_baseline(wl, dtype_name, target_s=12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
     import numpy as np
@@ -313,7 +323,10 @@ def run_ours(args):
                    "parallelism": f"dp{world} (batch-sharded, NCCL all-reduce of dW)",
                    "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak,
+                     "traffic": ncu_traffic(dom) if args.dtype == "f32" and args.angle is None else None,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, fp32 S1)",
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ab[dom]},
         "gpu_launches": launches, "clocks": ck, "e2e": e2e,
     }
