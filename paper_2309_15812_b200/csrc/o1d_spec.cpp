@@ -49,6 +49,7 @@ struct Driver {
     PFN_cuModuleGetFunction_v2000 moduleGetFunction = nullptr;
     PFN_cuFuncSetAttribute_v9000 funcSetAttribute = nullptr;
     PFN_cuLaunchKernel_v4000 launchKernel = nullptr;
+    PFN_cuLaunchKernelEx_v11060 launchKernelEx = nullptr;
     PFN_cuTensorMapEncodeTiled_v12000 encodeTiled = nullptr;
     PFN_cuGetErrorString_v6000 getErrorString = nullptr;
     std::string err;
@@ -74,7 +75,8 @@ Driver &drv() {
         bool ok = entry("cuModuleLoadData", &d.moduleLoadData, &e) && entry("cuModuleUnload", &d.moduleUnload, &e) &&
                   entry("cuModuleGetFunction", &d.moduleGetFunction, &e) &&
                   entry("cuFuncSetAttribute", &d.funcSetAttribute, &e) && entry("cuLaunchKernel", &d.launchKernel, &e) &&
-                  entry("cuTensorMapEncodeTiled", &d.encodeTiled, &e) && entry("cuGetErrorString", &d.getErrorString, &e);
+                  entry("cuTensorMapEncodeTiled", &d.encodeTiled, &e) && entry("cuGetErrorString", &d.getErrorString, &e) &&
+                  entry("cuLaunchKernelEx", &d.launchKernelEx, &e);
         if (!ok) d.err = e;
     });
     return d;
@@ -270,6 +272,10 @@ __device__ __forceinline__ float f2lo(u64 v) { float lo, hi; asm("mov.b64 {%0, %
 __device__ __forceinline__ float f2hi(u64 v) { float lo, hi; asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); return hi; }
 // packed fp32 FMA (two lanes per instruction, each fma.rn): d = a * b + c
 __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) { u64 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+// programmatic dependent launch: wait for the preceding grid (and its memory) before
+// touching global memory; allow the next grid to start launching when we run dry
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ u32 smid() { u32 r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 // 32 values per lane -> lane L returns the warp sum of v[L] (31 shuffles)
 __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
@@ -443,10 +449,33 @@ void emit_thread_map(std::ostringstream &os, const Ctx &x) {
 }
 
 // distinct taps of tap group gi (contiguous ranges of the distinct-tap list)
+// Estimated issue cost of a contiguous range of distinct taps for one 7x7 block:
+// 4 packed/scalar FMA instructions per (row, tap) + one LDS per footprint pixel.
+int range_cost(const Geo &g, int lo, int hi) {
+    std::set<std::pair<int, int>> px;
+    for (int d = lo; d < hi; ++d)
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) px.insert({r + g.taps[d].dh, s + g.taps[d].dw});
+    return 4 * R * (hi - lo) + (int)px.size();
+}
+
+// Distinct taps of tap group gi: contiguous ranges of the distinct-tap list whose
+// boundaries balance the estimated cost (groups run on different warps that
+// meet at the output combine, so the slowest group sets the pace).
 std::vector<int> group_taps(const Geo &g, int gi, int G) {
     const int nd = (int)g.taps.size();
+    std::vector<int> cut(G + 1, 0);
+    cut[G] = nd;
+    for (int q = 1; q < G; ++q) cut[q] = (q * nd) / G;
+    if (G == 2) {  // exact search of the single cut point
+        int best = 1 << 30;
+        for (int c = 1; c < nd; ++c) {
+            const int m = std::max(range_cost(g, 0, c), range_cost(g, c, nd));
+            if (m < best) best = m, cut[1] = c;
+        }
+    }
     std::vector<int> v;
-    for (int d = (gi * nd) / G; d < ((gi + 1) * nd) / G; ++d) v.push_back(d);
+    for (int d = cut[gi]; d < cut[gi + 1]; ++d) v.push_back(d);
     return v;
 }
 
@@ -673,6 +702,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "  if (warp == 0) {\n"
        << "    // ------------------------------------------------------------ producer\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "    pdl_wait();\n"
        << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
@@ -696,7 +726,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[b * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n"
        << "      if (lane == 0) s_item[b] = item;\n"
        << "      mbar_arrive(full + b);   // 32 producer arrivals (+ the tile bytes) complete the phase\n"
-       << "      if (item < 0) break;\n"
+       << "      if (item < 0) { pdl_trigger(); break; }\n"
        << "    }\n"
        << "    if (lane == 0) sched_exit(p.sched);\n"
        << "    return;\n"
@@ -913,6 +943,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  __syncthreads();\n"
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "    pdl_wait();\n"
        << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
@@ -935,7 +966,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "        }\n"
        << "      }\n"
        << "      mbar_arrive(full + b);\n"
-       << "      if (item < 0) break;\n"
+       << "      if (item < 0) { pdl_trigger(); break; }\n"
        << "    }\n"
        << "    if (lane == 0) sched_exit(p.sched);\n"
        << "    return;\n"
@@ -996,6 +1027,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     const int NE = x.N * x.wpg;
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
        << "  __shared__ double part[8][64];\n"
+       << "  pdl_wait();\n"
        << "  const int c = blockIdx.x, j = threadIdx.x >> 5 /* 0..7 */, lane = threadIdx.x & 31;\n"
        << "  const float* base = ws + (u64)c * " << NE << " * " << x.K << ";\n"
        << "  for (int k = lane; k < " << x.K << "; k += 32) {\n"
@@ -1237,13 +1269,29 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[4] = sp->d_sched + 3 * (nt + 1);
     ptrs[5] = dW;
     void *args[] = {blob};
-    CUresult r = drv().launchKernel(sp->fn[pass], (unsigned)sp->grid[pass], 1, 1, sp->threads[pass], 1, 1,
-                                    (unsigned)sp->smem[pass], static_cast<CUstream>(stream), args, nullptr);
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    const bool pdl = env_int("O1D_PDL", 1) != 0;
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = (unsigned)sp->grid[pass];
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = (unsigned)sp->threads[pass];
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)sp->smem[pass];
+    cfg.hStream = static_cast<CUstream>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CUresult r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
     if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of specialised kernel: " + cu_err(r));
     if (pass == 2) {
         const void *wsp = ws;
         void *fargs[] = {&wsp, &dW};
-        r = drv().launchKernel(sp->fin, (unsigned)d.C, 1, 1, 256, 1, 1, 0, static_cast<CUstream>(stream), fargs, nullptr);
+        CUlaunchConfig fc = cfg;
+        fc.gridDimX = (unsigned)d.C;
+        fc.blockDimX = 256;
+        fc.sharedMemBytes = 0;
+        r = drv().launchKernelEx(&fc, sp->fin, fargs, nullptr);
         if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of wgrad finalize: " + cu_err(r));
     }
     return O1D_OK;
