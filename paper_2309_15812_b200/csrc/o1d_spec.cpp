@@ -213,7 +213,7 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 }  // namespace
 
 struct SpecSet {
-    int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, PPC = 1, nt = 0, nsm = 0, gw = 1;
+    int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, nt = 0, nsm = 0, gw = 1;
     std::vector<Geo> fwd, bwd;  // per distinct table
     std::vector<int> count;     // planes per table
     CUmodule mod[3] = {nullptr, nullptr, nullptr};
@@ -291,53 +291,23 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
   }
   return v[0];
 }
-// Work scheduler (thread 0 only): per-table atomic counters handing out sets of
-// PPC consecutive planes; a CTA starts on its SM's home table (so co-resident
-// warps share one specialised code path in the instruction cache) and moves on
-// to the next table when it is exhausted.  `raw` is a counter value fetched one
-// set ahead, so the atomic's latency is hidden behind a whole set of compute.
-#ifdef GLOBAL_QUEUE
-// One queue over all planes in table-major order: at any moment the whole GPU
-// works on (at most two) consecutive tap tables, so the instruction footprint
-// in flight is one specialised code path, not NT of them.
-__device__ __forceinline__ int global_item(int g) {
-  int t = 0;
-  while (t < NT - 1 && g >= COUNT[t]) { g -= COUNT[t]; ++t; }
-  return (t << 22) | g;
-}
-__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
-  if (tcur < 0) return -1;
-  if (raw < (unsigned)TOTAL) return (int)raw;
-  tcur = -1;
-  return -1;
-}
-__device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
-  if (tcur >= 0) raw = atomicAdd(sched, (unsigned)PPC);
-}
-__device__ __forceinline__ int slot_item(int base, int q) {
-  if (base < 0 || base + q >= TOTAL) return -1;
-  return global_item(base + q);
-}
-#else
+// Work scheduler (producer lane 0): per-table atomic counters handing out
+// planes; a CTA starts on its SM's home table (so co-resident warps share one
+// specialised code path in the instruction cache) and moves on to the next
+// table when it is exhausted.  `raw` is a counter value fetched one plane
+// ahead, so the atomic's latency is hidden behind a whole plane of compute.
 __device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
   while (tcur >= 0) {
     if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
     if (++tried >= NT) { tcur = -1; break; }
     tcur = tcur + 1 == NT ? 0 : tcur + 1;
-    raw = atomicAdd(sched + tcur, (unsigned)PPC);
+    raw = atomicAdd(sched + tcur, 1u);
   }
   return -1;
 }
 __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
-  if (tcur >= 0) raw = atomicAdd(sched + tcur, (unsigned)PPC);
+  if (tcur >= 0) raw = atomicAdd(sched + tcur, 1u);
 }
-// item of plane slot q of a set whose first item is `base` (-1 when past the table's end)
-__device__ __forceinline__ int slot_item(int base, int q) {
-  if (base < 0) return -1;
-  const int t = base >> 22, i = (base & 0x3FFFFF) + q;
-  return i < COUNT[t] ? ((t << 22) | i) : -1;
-}
-#endif
 __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   t = item >> 22;
   const int i = item & 0x3FFFFF;
@@ -365,17 +335,16 @@ int env_int(const char *n, int dflt) {
 }
 
 struct Ctx {
-    int N, C, K, Ho, Wo, BR, BC, wpg, G, PPC, nt, nsm;  // wpg: warps per tap group; G: tap groups; PPC: planes per CTA
+    int N, C, K, Ho, Wo, BR, BC, wpg, G, nt, nsm;  // wpg: warps (bands) per tap group; G: tap groups
     bool ffma2 = false;                                  // packed fp32 FMA in the stencil
     int minb = 1;                                        // __launch_bounds__ min blocks per SM (stencil)
     int gw = 2;                                          // tap groups of the wgrad kernel
     int act = 0;                                         // activation dtype (o1d_dtype)
-    int nthreads() const { return 32 * wpg * G * PPC; }
-    int wpp() const { return wpg * G; }  // warps per plane slot
+    int nthreads() const { return 32 * wpg * G; }
 };
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
-    os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define PPC " << x.PPC << "\n";
+    os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n";
     // activation element type in shared memory / HBM; arithmetic is fp32 throughout
     if (x.act == O1D_F32)
         os << "typedef float act_t;\n#define LD(v) (v)\n"
@@ -388,12 +357,6 @@ void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &t
               "__device__ __forceinline__ float h2f(unsigned short h) { float f; asm(\"cvt.f32.f16 %0, %1;\" : \"=f\"(f) : \"h\"(h)); return f; }\n"
               "#define LD(v) h2f(v)\n"
               "__device__ __forceinline__ act_t to_act(float v) { unsigned short r; asm(\"cvt.rn.f16.f32 %0, %1;\" : \"=h\"(r) : \"f\"(v)); return r; }\n";
-    {
-        long tot = 0;
-        for (int t = 0; t < x.nt; ++t) tot += count[t];
-        os << "#define TOTAL " << tot << "\n";
-        if (env_int("O1D_HOME_MODE", 2) == 3) os << "#define GLOBAL_QUEUE 1\n";
-    }
     os << "__constant__ int COUNT[" << x.nt << "] = {";
     for (int t = 0; t < x.nt; ++t) os << (t ? "," : "") << count[t];
     os << "};\n";
@@ -409,46 +372,14 @@ void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &t
     os << "};\n__constant__ short CHLIST[" << x.C << "] = {";
     for (int c = 0; c < x.C; ++c) os << (c ? "," : "") << chlist[c];
     os << "};\n";
-    // home table per SM: SMs split among tables in proportion to their planes
-    long total = 0;
-    for (int t = 0; t < x.nt; ++t) total += count[t];
+    // home table per SM: (smid / 2) mod NT, i.e. both SMs of a TPC pair share one
+    // table (measured best of: contiguous smid ranges, smid mod NT, global
+    // table-major queue; the instruction cache is shared beyond one SM)
     os << "__constant__ unsigned char HOME[" << x.nsm << "] = {";
-    const int mode = env_int("O1D_HOME_MODE", 2);
-    long acc = 0;
-    int t = 0;
-    for (int s = 0; s < x.nsm; ++s) {
-        // mode 0: contiguous smid ranges per table, proportional to the table's planes;
-        // mode 1: smid mod NT; mode 2: (smid / 2) mod NT (TPC pairs)
-        int h;
-        if (mode == 3) {
-            h = 0;  // global table-major queue
-        } else if (mode == 1) {
-            h = s % x.nt;
-        } else if (mode == 2) {
-            h = (s / 2) % x.nt;
-        } else {
-            const double pos = (s + 0.5) * (double)total / x.nsm;
-            while (t < x.nt - 1 && pos >= acc + count[t]) acc += count[t], ++t;
-            h = t;
-        }
-        os << (s ? "," : "") << h;
-    }
+    for (int s = 0; s < x.nsm; ++s) os << (s ? "," : "") << (s / 2) % x.nt;
     os << "};\n" << kPrelude;
 }
 
-// thread -> (plane slot, tap group, 7x7 block): lanes cover 8 block-columns x 4 block-rows
-void emit_thread_map(std::ostringstream &os, const Ctx &x) {
-    const int bcg = (x.BC + 7) / 8;
-    os << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
-       << "  const int pp = warp / " << x.wpp() << ", grp = (warp / " << x.wpg << ") % " << x.G
-       << ", wg = warp % " << x.wpg << ";\n"
-       << "  const int ptid = tid - pp * " << 32 * x.wpp() << ";  // thread index within the plane slot\n"
-       << "  int bc = (lane & 7) + 8 * (wg % " << bcg << "), br = (lane >> 3) + 4 * (wg / " << bcg << ");\n"
-       << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
-       << "  if (!active) { bc = 0; br = 0; }\n";
-}
-
-// distinct taps of tap group gi (contiguous ranges of the distinct-tap list)
 // Estimated issue cost of a contiguous range of distinct taps for one 7x7 block:
 // 4 packed/scalar FMA instructions per (row, tap) + one LDS per footprint pixel.
 int range_cost(const Geo &g, int lo, int hi) {
@@ -518,74 +449,6 @@ size_t tile_bytes_of(const std::vector<Geo> &geo) {
 size_t stage_bytes_of(const Ctx &x) {
     const int rows = ((x.BR * R + 4 * R - 1) / (4 * R)) * (4 * R);  // whole 4*7-row bands
     return ((size_t)rows * x.Wo * 4 + 1023) & ~(size_t)1023;
-}
-
-// Shared-memory layout (both kernels):
-//   tiles [2 sets][PPC] | stage [PPC] (stencil only) | wsm [2][PPC][64] | bar [2] | s_item [2][PPC] | red
-struct Layout {
-    size_t TB, tiles, stage, wsm, bar, sitem, red, total;
-};
-Layout layout_of(const Ctx &x, const std::vector<Geo> &geo, bool stage, size_t red_bytes) {
-    Layout L;
-    L.TB = tile_bytes_of(geo);
-    L.tiles = 0;
-    L.stage = 2 * x.PPC * L.TB;
-    L.wsm = L.stage + (stage ? x.PPC * stage_bytes_of(x) : 0);
-    L.bar = L.wsm + 2 * x.PPC * 64 * 4;
-    L.sitem = L.bar + 16;
-    L.red = (L.sitem + 8 * x.PPC + 15) & ~(size_t)15;
-    L.total = L.red + red_bytes;
-    return L;
-}
-
-// Scheduling block run by warp 0 once the CTA finished reading buffer set b:
-// resolve the prefetched counter into the next set of PPC items, stage their
-// weights and issue their TMA loads (one mbarrier per set).
-void emit_schedule(std::ostringstream &os, const Ctx &x, const std::vector<Geo> &geo, const Layout &L,
-                   const std::string &b, bool weights, const std::string &ind) {
-    os << ind << "if (warp == 0) {\n"
-       << ind << "  int base = -1;\n"
-       << ind << "  if (lane == 0) { base = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
-       << ind << "  base = __shfl_sync(0xffffffffu, base, 0);\n"
-       << ind << "  int* si = s_item + (" << b << ") * PPC;\n"
-       << ind << "  if (lane < PPC) si[lane] = slot_item(base, lane);\n"
-       << ind << "  if (base >= 0) {\n";
-    if (weights)
-        os << ind << "    for (int e = lane; e < PPC * " << x.K << "; e += 32) {\n"
-           << ind << "      const int q = e / " << x.K << ", k = e - q * " << x.K << ";\n"
-           << ind << "      const int itq = slot_item(base, q);\n"
-           << ind << "      if (itq >= 0) { int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
-           << ind << "        wsm[((" << b << ") * PPC + q) * 64 + k] = __ldg(p.w + cq * " << x.K << " + k); }\n"
-           << ind << "    }\n";
-    os << ind << "    if (lane == 0) {\n"
-       << ind << "      unsigned bytes = 0;\n"
-       << ind << "      for (int q = 0; q < PPC; ++q) { const int itq = slot_item(base, q); if (itq < 0) break;\n"
-       << ind << "        switch (itq >> 22) {\n";
-    for (int t = 0; t < x.nt; ++t) os << ind << "        case " << t << ": bytes += " << geo[t].bytes << "u; break;\n";
-    os << ind << "        }\n" << ind << "      }\n"
-       << ind << "      mbar_expect(bar + (" << b << "), bytes);\n"
-       << ind << "      for (int q = 0; q < PPC; ++q) { const int itq = slot_item(base, q); if (itq < 0) break;\n"
-       << ind << "        int tq, cq, nq; item_cn(itq, tq, cq, nq);\n"
-       << ind << "        float* dst = reinterpret_cast<float*>(smem + ((" << b << ") * PPC + q) * " << L.TB << ");\n"
-       << ind << "        switch (tq) {\n";
-    for (int t = 0; t < x.nt; ++t)
-        os << ind << "        case " << t << ": tma_load(dst, &p.in_map[" << t << "], " << geo[t].x0 << ", "
-           << geo[t].minDH << ", cq, nq, bar + (" << b << ")); break;\n";
-    os << ind << "        }\n" << ind << "      }\n" << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
-}
-
-// prologue: barriers, the first two sets, their weights and TMA loads
-void emit_prologue(std::ostringstream &os, const Ctx &x, const std::vector<Geo> &geo, const Layout &L, bool weights) {
-    os << "  float* wsm = reinterpret_cast<float*>(smem + " << L.wsm << ");\n"
-       << "  u64* bar = reinterpret_cast<u64*>(smem + " << L.bar << ");\n"
-       << "  int* s_item = reinterpret_cast<int*>(smem + " << L.sitem << ");\n"
-       << "  int tcur = 0, tried = 0; unsigned raw = 0;\n"
-       << "  if (tid == 0) {\n    mbar_init(bar, 1); mbar_init(bar + 1, 1); fence_mbar_init();\n"
-       << "    tcur = HOME[smid() % " << x.nsm << "];\n    raw = atomicAdd(p.sched + tcur, (unsigned)PPC);\n  }\n"
-       << "  __syncthreads();\n";
-    emit_schedule(os, x, geo, L, "0", weights, "  ");
-    emit_schedule(os, x, geo, L, "1", weights, "  ");
-    os << "  __syncthreads();\n";
 }
 
 // Stencil taps of group `ds` with packed FFMA2: output columns are paired
@@ -703,7 +566,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    // ------------------------------------------------------------ producer\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      // buffer b is free once every consumer warp released item it-2: a named\n"
@@ -944,7 +807,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, (unsigned)PPC); }\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
@@ -1086,9 +949,8 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     const int bcg = (sp->BC + 7) / 8, brg = (sp->BR + 3) / 4;
     sp->wpg = bcg * brg;
     sp->G = env_int("O1D_G", (sp->wpg <= 2 && d.K >= 8) ? 2 : 1);  // tap groups per plane
-    sp->PPC = env_int("O1D_PPC", 1);                                 // planes per CTA
-    if (sp->G < 1 || sp->G > 4 || sp->PPC < 1 || sp->PPC > 8) return false;
-    sp->nthreads = 32 * sp->wpg * sp->G * sp->PPC;
+    if (sp->G < 1 || sp->G > 2) return false;
+    sp->nthreads = 32 * sp->wpg * sp->G;
     sp->nt = pl->n_distinct;
     sp->nsm = nsm;
     std::vector<int> rep(sp->nt, -1);  // one representative channel per distinct table
@@ -1106,7 +968,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     }
     if (d.W > 256 || d.H > 256 || sp->nthreads > 1024) return false;
     if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
-    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
     x.act = d.dtype;
     x.minb = env_int("O1D_MINB", 3);
@@ -1169,7 +1031,7 @@ o1d_status spec_create(o1d_plan *pl) {
             delete sp;
             return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
         }
-    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->PPC, sp->nt, nsm};
+    Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.act = d.dtype;
     sp->smem[0] = stencil_smem(x, sp->fwd);
     sp->smem[1] = stencil_smem(x, sp->bwd);
@@ -1182,7 +1044,7 @@ o1d_status spec_create(o1d_plan *pl) {
     PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occ = nullptr;
     std::string e;
     entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", &occ, &e);
-    const long planes = ((long)d.N * d.C + sp->PPC - 1) / sp->PPC;
+    const long planes = (long)d.N * d.C;
     for (int i = 0; i < 3; ++i) {
         CUresult r = dr.moduleLoadData(&sp->mod[i], cubin[i].data());
         if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&sp->fn[i], sp->mod[i], fnames[i]);
@@ -1215,9 +1077,9 @@ o1d_status spec_create(o1d_plan *pl) {
     pl->spec = sp;
     char buf[768];
     snprintf(buf, sizeof buf,
-             "spec(persistent, 7x7 blocks, %d threads/CTA (%d planes x %d tap groups), %d tap tables, TMA 4-D double-buffered; "
+             "spec(persistent warp-specialised, 7x7 blocks, %d consumer threads/CTA (%d tap groups), %d tap tables, TMA 4-D double-buffered; "
              "fwd grid %d smem %zu [%s]; bwd_in grid %d [%s]; wgrad grid %d smem %zu [%s])",
-             sp->nthreads, sp->PPC, sp->G, sp->nt, sp->grid[0], sp->smem[0], sp->regs[0].c_str(), sp->grid[1], sp->regs[1].c_str(),
+             sp->nthreads, sp->G, sp->nt, sp->grid[0], sp->smem[0], sp->regs[0].c_str(), sp->grid[1], sp->regs[1].c_str(),
              sp->grid[2], sp->smem[2], sp->regs[2].c_str());
     pl->describe = buf;
     if (env_flag("O1D_VERBOSE")) fprintf(stderr, "[o1d] %s\n", buf);

@@ -117,6 +117,15 @@ def test_full_stage1_config(dtype):
     print(plan.describe(), errs)
 
 
+@pytest.mark.parametrize("K", [7, 31, 63])
+def test_full_ksweep_config(K):
+    """BASELINE configs[2] (N=128, C=384, 14x14, D=8) at full size."""
+    wl = inputs.ksweep(K)
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan, errs = run_case(wl.N, wl.C, wl.H, wl.W, wl.K, angles, 1, torch.float32, 0)
+    print(plan.describe(), errs)
+
+
 def test_errors_on_gpu():
     plan = B.Plan(1, 8, 14, 14, 7, np.zeros(8), device="cuda:0")
     x = torch.zeros(1, 8, 14, 14, device="cuda:0")
