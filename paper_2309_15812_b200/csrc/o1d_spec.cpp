@@ -170,10 +170,10 @@ struct Geo {  // one distinct tap table, one pass
     std::vector<Tap> taps;
     std::vector<int> k2d;  // k -> distinct index
     int minDH, maxDH, minDW, maxDW;
-    int rows, pitch;       // TMA box (rows x pitch floats) = shared-memory tile
-    int x0;                // first tile column (image coords), 16-byte aligned: TMA needs an
-                           // aligned innermost start coordinate
-    uint32_t bytes;
+    int rows, pitch;       // TMA box (rows x pitch elements) = shared-memory tile
+    int x0;                // first tile column in image coordinates (0: see make_geo)
+    int guard;             // bytes of zeros in front of the tile (>= one pitch, 128-aligned)
+    uint32_t bytes;        // TMA box bytes
 };
 
 int pitch_for(int cols) {
@@ -182,7 +182,13 @@ int pitch_for(int cols) {
     return p;
 }
 
-Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, int BC, int es) {
+// Tile geometry.  The box starts at image column 0 and is `pitch` wide, so the
+// columns past the image edge are zero-filled by the TMA unit; a read left of
+// column 0 wraps to the previous row's zero columns (pitch >= Win - minDW), and
+// a zero guard row in front of the tile serves the first row.  The left halo
+// therefore costs no shared memory, and the innermost TMA start coordinate is
+// always 0 (TMA needs a 16-byte-aligned innermost start).
+Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, int BC, int es, int Win) {
     Geo g;
     std::map<std::pair<int, int>, int> idx;
     g.k2d.resize(K);
@@ -202,11 +208,11 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
         g.minDW = std::min(g.minDW, dw);
         g.maxDW = std::max(g.maxDW, dw);
     }
-    const int vec = 16 / es;
-    g.x0 = g.minDW >= 0 ? (g.minDW / vec) * vec : -((-g.minDW + vec - 1) / vec) * vec;
+    g.x0 = 0;
     g.rows = R * BR + (g.maxDH - g.minDH);
-    g.pitch = pitch_for(S * BC + (g.maxDW - g.x0));
+    g.pitch = pitch_for(std::max(Win - std::min(g.minDW, 0), S * BC + std::max(g.maxDW, 0)));
     g.bytes = (uint32_t)(g.rows * g.pitch * es);
+    g.guard = ((g.pitch * es) + 127) & ~127;
     return g;
 }
 
@@ -442,7 +448,7 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
 
 size_t tile_bytes_of(const std::vector<Geo> &geo) {
     size_t b = 0;
-    for (auto &g : geo) b = std::max(b, (size_t)g.bytes);
+    for (auto &g : geo) b = std::max(b, (size_t)g.guard + g.bytes);
     return (b + 1023) & ~(size_t)1023;
 }
 
@@ -557,6 +563,9 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "  u64* const empty = full + 2;\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  for (int i = threadIdx.x; i < 2 * " << TB / 16 << "; i += blockDim.x) {  // zero guards (and tiles)\n"
+       << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
+       << "  }\n"
        << "  if (tid == 0) {\n"
        << "    mbar_init(full, 32); mbar_init(full + 1, 32);\n"
 
@@ -578,11 +587,11 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "      int t2 = 0, c2 = 0, n2 = 0;\n"
        << "      if (item >= 0) item_cn(item, t2, c2, n2);\n"
        << "      if (lane == 0 && item >= 0) {   // issue the tile load first: it is the long pole\n"
-       << "        float* dst = reinterpret_cast<float*>(smem + b * " << TB << ");\n"
+       << "        unsigned char* dst = smem + b * " << TB << ";\n"
        << "        switch (t2) {\n";
     for (int t = 0; t < x.nt; ++t)
-        os << "        case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes << "u); tma_load(dst, &p.in_map[" << t
-           << "], " << geo[t].x0 << ", " << geo[t].minDH << ", c2, n2, full + b); break;\n";
+        os << "        case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes << "u); tma_load(dst + " << geo[t].guard
+           << ", &p.in_map[" << t << "], " << geo[t].x0 << ", " << geo[t].minDH << ", c2, n2, full + b); break;\n";
     os << "        }\n"
        << "      }\n"
        << "      if (item >= 0)\n"
@@ -609,7 +618,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const act_t* tile = reinterpret_cast<const act_t*>(smem + b * " << TB << ");\n"
+       << "    const unsigned char* tile = smem + b * " << TB << ";\n"
        << "    const float* wv = wsm + b * 64;\n";
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
@@ -617,7 +626,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const act_t* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile + " << g.guard << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < x.G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
@@ -802,6 +811,8 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  for (int i = threadIdx.x; i < 2 * " << TB / 16 << "; i += blockDim.x)  // zero guards (and tiles)\n"
+       << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
        << "  if (tid == 0) { mbar_init(full, 32); mbar_init(full + 1, 32); fence_mbar_init(); }\n"
        << "  __syncthreads();\n"
        << "  if (warp == 0) {\n"
@@ -818,11 +829,11 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "        s_item[b] = item;\n"
        << "        if (item >= 0) {\n"
        << "          int t2, c2, n2; item_cn(item, t2, c2, n2);\n"
-       << "          float* dst = reinterpret_cast<float*>(smem + b * " << TB << ");\n"
+       << "          unsigned char* dst = smem + b * " << TB << ";\n"
        << "          switch (t2) {\n";
     for (int t = 0; t < x.nt; ++t)
         os << "          case " << t << ": mbar_expect_tx(full + b, " << geo[t].bytes + (uint32_t)(dyp * dyrows * es)
-           << "u); tma_load(dst, &p.in_map[" << t << "], " << geo[t].x0 << ", " << geo[t].minDH
+           << "u); tma_load(dst + " << geo[t].guard << ", &p.in_map[" << t << "], " << geo[t].x0 << ", " << geo[t].minDH
            << ", c2, n2, full + b); break;\n";
     os << "          }\n"
        << "          tma_load(smem + " << off_dy << " + b * " << DB << ", &p.out_map, 0, 0, c2, n2, full + b);\n"
@@ -845,7 +856,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const act_t* tile = reinterpret_cast<const act_t*>(smem + b * " << TB << ");\n"
+       << "    const unsigned char* tile = smem + b * " << TB << ";\n"
        << "    const act_t* gb = reinterpret_cast<const act_t*>(smem + " << off_dy << " + b * " << DB << ") + (" << R
        << " * br) * " << dyp << " + " << S << " * bc;\n";
     for (int r = 0; r < R; ++r)
@@ -856,7 +867,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const act_t* tb = tile + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile + " << g.guard << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
@@ -961,8 +972,8 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     }
     for (int t = 0; t < sp->nt; ++t) {
         const int c = rep[t];
-        sp->fwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, false, sp->BR, sp->BC, es));
-        sp->bwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, true, sp->BR, sp->BC, es));
+        sp->fwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, false, sp->BR, sp->BC, es, d.W));
+        sp->bwd.push_back(make_geo(&pl->oh[(size_t)c * d.K], &pl->ow[(size_t)c * d.K], d.K, true, sp->BR, sp->BC, es, pl->Q));
         for (const Geo *g : {&sp->fwd.back(), &sp->bwd.back()})
             if (g->pitch > 256 || g->rows > 256 || g->bytes > 100 * 1024) return false;
     }
