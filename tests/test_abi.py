@@ -96,3 +96,31 @@ def test_error_codes():
         assert st == status, (fields, st, L.o1d_last_error())
         assert not h.value
     assert L.o1d_forward(None, None, None, None, None) == 1
+
+
+@pytest.mark.parametrize("pass_id", [0, 1, 2])
+def test_spec_source_compiles_for_sm100a(tmp_path, pass_id):
+    """The runtime-generated specialised kernels are valid sm_100a CUDA (host-only
+    generation through the ABI, compiled here with nvcc; no GPU needed)."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    src = B.spec_source(2, 16, 56, 56, 15, T.direction_angles(8, 16, "cycled"), pass_id)
+    assert "o1d_" in src and "cp.async.bulk.tensor" in src
+    f = tmp_path / f"k{pass_id}.cu"
+    f.write_text(src)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-o", str(tmp_path / "k.cubin"),
+                        str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    sass = subprocess.run(["cuobjdump", "-sass", str(tmp_path / "k.cubin")], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass  # TMA tile loads
+    if pass_id < 2:
+        assert "FFMA2" in sass and "UTMASTG" in sass  # packed FP32 + TMA stores
+
+
+def test_spec_source_ineligible_shapes():
+    with pytest.raises(B.O1DError) as e:
+        B.spec_source(1, 8, 14, 14, 7, np.zeros(8), 0)  # 14*4 B rows are not TMA-legal
+    assert e.value.status == 5
+    with pytest.raises(B.O1DError):
+        B.spec_source(1, 8, 56, 56, 7, np.zeros(8), 0, stride=2)
