@@ -312,3 +312,100 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
 }
 
 }  // namespace o1d
+
+// ----------------------------------------------------------------------------
+// GPC topology probe.  The instruction cache is shared beyond one SM, so the
+// specialised kernels give every GPC its own tap table ("home" table).  CTAs of
+// one thread-block cluster always share a GPC; the probe launches many
+// clusters and unions the %smid sets they land on.  Result: gpc id per smid
+// (-1 for ids never observed).  Cached per device.
+// ----------------------------------------------------------------------------
+#include <map>
+#include <mutex>
+#include <numeric>
+
+namespace o1d {
+namespace {
+__global__ void smid_probe_kernel(int *out) {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    if (threadIdx.x == 0) out[blockIdx.x] = (int)s;
+    const long long t0 = clock64();
+    while (clock64() - t0 < 20000) {
+    }
+}
+
+int uf_find(std::vector<int> &p, int x) {
+    while (p[x] != x) x = p[x] = p[p[x]];
+    return x;
+}
+}  // namespace
+
+bool gpc_map(int device, std::vector<int> *gpc_of_smid) {
+    static std::mutex mu;
+    static std::map<int, std::vector<int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) {
+        *gpc_of_smid = it->second;
+        return !it->second.empty();
+    }
+    std::vector<int> result;
+    int *d = nullptr;
+    const int MAXS = 1024;
+    if (cudaMalloc(&d, sizeof(int) * 16 * 256) == cudaSuccess) {
+        cudaFuncSetAttribute(smid_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        std::vector<int> par(MAXS), seen(MAXS, 0);
+        std::iota(par.begin(), par.end(), 0);
+        bool ok = false;
+        for (int cs : {16, 8, 4, 2}) {
+            for (int rep = 0; rep < 24; ++rep) {
+                cudaLaunchConfig_t cfg = {};
+                const int ncl = 160 / cs + rep % 5;
+                cfg.gridDim = dim3(cs * ncl);
+                cfg.blockDim = dim3(32);
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = cs;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                if (cudaLaunchKernelEx(&cfg, smid_probe_kernel, d) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+                    cudaGetLastError();
+                    break;
+                }
+                std::vector<int> c(cs * ncl);
+                if (cudaMemcpy(c.data(), d, sizeof(int) * c.size(), cudaMemcpyDeviceToHost) != cudaSuccess) break;
+                ok = true;
+                for (int k = 0; k < ncl; ++k)
+                    for (int j = 0; j < cs; ++j) {
+                        const int s = c[k * cs + j], s0 = c[k * cs];
+                        if (s < 0 || s >= MAXS || s0 < 0 || s0 >= MAXS) continue;
+                        seen[s] = 1;
+                        par[uf_find(par, s)] = uf_find(par, s0);
+                    }
+            }
+        }
+        cudaFree(d);
+        if (ok) {
+            int maxs = 0;
+            for (int s = 0; s < MAXS; ++s)
+                if (seen[s]) maxs = s;
+            result.assign(maxs + 1, -1);
+            std::map<int, int> ids;
+            for (int s = 0; s <= maxs; ++s)
+                if (seen[s]) {
+                    const int r = uf_find(par, s);
+                    auto f = ids.find(r);
+                    if (f == ids.end()) f = ids.emplace(r, (int)ids.size()).first;
+                    result[s] = f->second;
+                }
+        }
+    }
+    cudaGetLastError();
+    cache[device] = result;
+    *gpc_of_smid = result;
+    return !result.empty();
+}
+}  // namespace o1d

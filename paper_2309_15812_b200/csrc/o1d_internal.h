@@ -66,4 +66,6 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
                               void *stream);
 int generic_band_rows(const o1d_plan *pl, const Stencil &st, int extra_rows_per_out);
 size_t dtype_size(int dt);
+// GPC id per %smid (probe with thread-block clusters; cached); false if unavailable
+bool gpc_map(int device, std::vector<int> *gpc_of_smid);
 }  // namespace o1d

@@ -346,6 +346,7 @@ struct Ctx {
     int minb = 1;                                        // __launch_bounds__ min blocks per SM (stencil)
     int gw = 2;                                          // tap groups of the wgrad kernel
     int act = 0;                                         // activation dtype (o1d_dtype)
+    std::vector<int> home;                               // home table per %smid (empty: TPC-pair fallback)
     int nthreads() const { return 32 * wpg * G; }
 };
 
@@ -378,11 +379,11 @@ void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &t
     os << "};\n__constant__ short CHLIST[" << x.C << "] = {";
     for (int c = 0; c < x.C; ++c) os << (c ? "," : "") << chlist[c];
     os << "};\n";
-    // home table per SM: (smid / 2) mod NT, i.e. both SMs of a TPC pair share one
-    // table (measured best of: contiguous smid ranges, smid mod NT, global
-    // table-major queue; the instruction cache is shared beyond one SM)
-    os << "__constant__ unsigned char HOME[" << x.nsm << "] = {";
-    for (int s = 0; s < x.nsm; ++s) os << (s ? "," : "") << (s / 2) % x.nt;
+    // home table per SM (see home_tables()); fallback without a topology probe:
+    // (smid / 2) mod NT, i.e. TPC pairs share a table
+    const int nh = x.home.empty() ? x.nsm : (int)x.home.size();
+    os << "#define NHOME " << nh << "\n__constant__ unsigned char HOME[" << nh << "] = {";
+    for (int s = 0; s < nh; ++s) os << (s ? "," : "") << (x.home.empty() ? (s / 2) % x.nt : x.home[s]);
     os << "};\n" << kPrelude;
 }
 
@@ -575,7 +576,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    // ------------------------------------------------------------ producer\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      // buffer b is free once every consumer warp released item it-2: a named\n"
@@ -818,7 +819,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % " << x.nsm << "]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { tcur = HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
@@ -947,9 +948,53 @@ o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int 
 
 }  // namespace
 
+// Home tap table of every SM.  The instruction cache is shared within a GPC
+// (measured: per-SM and per-TPC homes still thrash when neighbouring TPCs run
+// other tables), so SMs are ordered GPC by GPC (gpc_map probe) and each table
+// gets a contiguous run of TPC pairs proportional to its planes: a table spans
+// ~one GPC for D = 8.  mode 1: whole GPCs greedily (never split a GPC).
+std::vector<int> home_tables(const std::vector<int> &gpc_of_smid, const std::vector<int> &count, int nt) {
+    const int n = (int)gpc_of_smid.size();
+    std::vector<int> home(n, 0);
+    std::map<int, std::vector<int>> groups;  // gpc -> smids (unknown ids: own group)
+    for (int s = 0; s < n; ++s) groups[gpc_of_smid[s] >= 0 ? gpc_of_smid[s] : 100000 + s].push_back(s);
+    long total = 0;
+    for (int t = 0; t < nt; ++t) total += count[t];
+    const int mode = env_int("O1D_HOME_MODE", 0);
+    if (mode == 1 && (int)groups.size() >= nt) {
+        std::vector<std::pair<int, int>> order;  // (size, gpc)
+        for (auto &g : groups) order.push_back({-(int)g.second.size(), g.first});
+        std::sort(order.begin(), order.end());
+        std::vector<double> assigned(nt, 0.0);
+        for (auto &o : order) {
+            int best = 0;
+            double bd = -1;
+            for (int t = 0; t < nt; ++t) {
+                const double deficit = count[t] / (assigned[t] + 1e-9);
+                if (deficit > bd) bd = deficit, best = t;
+            }
+            assigned[best] += -o.first;
+            for (int sm : groups[o.second]) home[sm] = best;
+        }
+        return home;
+    }
+    std::vector<int> ordered;
+    for (auto &g : groups) ordered.insert(ordered.end(), g.second.begin(), g.second.end());
+    long acc = 0;
+    int t = 0;
+    const int m = (int)ordered.size();
+    for (int i = 0; i < m; i += 2) {  // TPC pairs stay together
+        const double pos = (i + 1.0) * (double)total / m;
+        while (t < nt - 1 && pos >= acc + count[t]) acc += count[t], ++t;
+        home[ordered[i]] = t;
+        if (i + 1 < m) home[ordered[i + 1]] = t;
+    }
+    return home;
+}
+
 // Host-only part: eligibility, geometry and generated sources (no CUDA calls).
 // Returns false (and no sources) when the plan is not eligible.
-bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) {
+bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, const std::vector<int> *gpc) {
     const o1d_desc &d = pl->d;
     const int es = (int)dtype_size(d.dtype);
     if (d.stride != 1) return false;
@@ -982,6 +1027,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm) 
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
     x.act = d.dtype;
+    if (gpc && !gpc->empty()) x.home = home_tables(*gpc, sp->count, sp->nt);
     x.minb = env_int("O1D_MINB", 3);
     x.gw = env_int("O1D_GW", 2);
     if (x.gw < 1 || x.gw > 8) return false;
@@ -1014,7 +1060,9 @@ o1d_status spec_create(o1d_plan *pl) {
         return fail(O1D_CUDA_ERROR, "cannot query the SM count");
     SpecSet *sp = new SpecSet();
     std::string src[3];
-    if (!spec_prepare(pl, sp, src, nsm)) {
+    std::vector<int> gpc;
+    if (!gpc_map(pl->device, &gpc)) gpc.clear();
+    if (!spec_prepare(pl, sp, src, nsm, &gpc)) {
         delete sp;
         return O1D_OK;
     }
@@ -1174,7 +1222,7 @@ o1d_status spec_source(const o1d_plan *pl, int pass, std::string *out) {
     SpecSet sp;
     std::string src[3];
     if (pass < 0 || pass > 2) return fail(O1D_INVALID_ARG, "pass must be 0, 1 or 2");
-    if (!spec_prepare(pl, &sp, src, 148)) return fail(O1D_UNSUPPORTED, "plan is not eligible for specialised kernels");
+    if (!spec_prepare(pl, &sp, src, 148, nullptr)) return fail(O1D_UNSUPPORTED, "plan is not eligible for specialised kernels");
     *out = src[pass];
     return O1D_OK;
 }
