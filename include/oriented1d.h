@@ -145,9 +145,11 @@ O1D_API o1d_status o1d_backward_weight(const o1d_plan *plan, const void *x, cons
 
 /* One training step of the layer through HOST buffers (the end-to-end path):
  * copies x, w, dy host->device, runs forward, backward_input and
- * backward_weight, copies y, dx, dW device->host, all on `stream`, then
- * synchronises the stream.  Host buffers should be pinned for asynchronous
- * copies.  dev_ws: device scratch of >= o1d_step_host_workspace_bytes(plan)
+ * backward_weight, copies y, dx, dW device->host, then synchronises `stream`.
+ * The plan's internal second stream overlaps the two PCIe directions with each
+ * other and with the kernels (forward + D2H y on `stream`; H2D dy,
+ * backward_input, D2H dx, backward_weight, D2H dW on the second stream); calls
+ * on one plan must not run concurrently.  Host buffers should be pinned.  dev_ws: device scratch of >= o1d_step_host_workspace_bytes(plan)
  * bytes (holds device copies of every tensor and the dW workspace). */
 O1D_API size_t o1d_step_host_workspace_bytes(const o1d_plan *plan);
 O1D_API o1d_status o1d_step_host(const o1d_plan *plan, const void *x_h, const float *w_h, const void *dy_h,

@@ -227,6 +227,19 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
         return fail(O1D_UNSUPPORTED, "image row (plus halo) does not fit in shared memory");
     }
     pl->bw_bands = (pl->P + pl->bw_band - 1) / pl->bw_band;
+    {
+        cudaStream_t s2 = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess) {
+            o1d_plan_destroy(pl);
+            return fail(O1D_CUDA_ERROR, "stream/event creation failed");
+        }
+        pl->aux_stream = s2;
+        pl->aux_ev[0] = e0;
+        pl->aux_ev[1] = e1;
+    }
     pl->ws_bytes = sizeof(float) * (size_t)d->N * C * pl->bw_bands * K;
     char buf[256];
     snprintf(buf, sizeof buf, "generic(fwd band %d, bwd_in band %d, bwd_w band %d), %d distinct tap tables",
@@ -246,6 +259,9 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
 void o1d_plan_destroy(o1d_plan *pl) {
     if (!pl) return;
     spec_destroy(pl);
+    if (pl->aux_stream) cudaStreamDestroy(static_cast<cudaStream_t>(pl->aux_stream));
+    for (void *e : pl->aux_ev)
+        if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
     if (pl->d_block) cudaFree(pl->d_block);
     delete pl;
 }
@@ -342,6 +358,7 @@ o1d_status o1d_step_host(const o1d_plan *pl, const void *x_h, const float *w_h, 
     if (o1d_status st = check_ptr(dev_ws, "dev_ws")) return st;
     if (dev_ws_bytes < o1d_step_host_workspace_bytes(pl))
         return fail(O1D_WORKSPACE_TOO_SMALL, "dev_ws_bytes < o1d_step_host_workspace_bytes(plan)");
+    if (o1d_status st = check_device(pl)) return st;
     const size_t es = dtype_size(pl->d.dtype);
     const size_t nx = (size_t)pl->d.N * pl->d.C * pl->d.H * pl->d.W * es;
     const size_t ny = (size_t)pl->d.N * pl->d.C * pl->P * pl->Q * es;
@@ -354,21 +371,31 @@ o1d_status o1d_step_host(const o1d_plan *pl, const void *x_h, const float *w_h, 
     float *w = reinterpret_cast<float *>(b); b += align256(nw);
     float *dW = reinterpret_cast<float *>(b); b += align256(nw);
     void *ws = b;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (cudaMemcpyAsync(x, x_h, nx, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(w, w_h, nw, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(dy, dy_h, ny, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return fail(O1D_CUDA_ERROR, std::string("H2D: ") + cudaGetErrorString(cudaGetLastError()));
+    // Two streams so the PCIe directions overlap with each other and with the
+    // kernels:  s  : H2D w, x  -> forward        -> D2H y
+    //           s2 : H2D dy    -> backward_input -> D2H dx -> (x ready) backward_weight -> D2H dW
+    cudaStream_t s = static_cast<cudaStream_t>(stream), s2 = static_cast<cudaStream_t>(pl->aux_stream);
+    cudaEvent_t e_in = static_cast<cudaEvent_t>(pl->aux_ev[0]), e_out = static_cast<cudaEvent_t>(pl->aux_ev[1]);
+    auto cu = [](cudaError_t e, const char *what) -> o1d_status {
+        if (e != cudaSuccess) return fail(O1D_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+        return O1D_OK;
+    };
+    if (o1d_status st = cu(cudaEventRecord(e_out, s), "event")) return st;  // s2 starts after prior work on s
+    if (o1d_status st = cu(cudaStreamWaitEvent(s2, e_out, 0), "wait")) return st;
+    if (o1d_status st = cu(cudaMemcpyAsync(w, w_h, nw, cudaMemcpyHostToDevice, s), "H2D w")) return st;
+    if (o1d_status st = cu(cudaMemcpyAsync(x, x_h, nx, cudaMemcpyHostToDevice, s), "H2D x")) return st;
+    if (o1d_status st = cu(cudaEventRecord(e_in, s), "event")) return st;
+    if (o1d_status st = cu(cudaMemcpyAsync(dy, dy_h, ny, cudaMemcpyHostToDevice, s2), "H2D dy")) return st;
     if (o1d_status st = o1d_forward(pl, x, w, y, stream)) return st;
-    if (o1d_status st = o1d_backward_input(pl, dy, w, dx, stream)) return st;
-    if (o1d_status st = o1d_backward_weight(pl, x, dy, dW, ws, o1d_workspace_bytes(pl), stream)) return st;
-    if (cudaMemcpyAsync(y_h, y, ny, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(dx_h, dx, nx, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(dW_h, dW, nw, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return fail(O1D_CUDA_ERROR, std::string("D2H: ") + cudaGetErrorString(cudaGetLastError()));
-    if (cudaStreamSynchronize(s) != cudaSuccess)
-        return fail(O1D_CUDA_ERROR, std::string("o1d_step_host: ") + cudaGetErrorString(cudaGetLastError()));
-    return O1D_OK;
+    if (o1d_status st = cu(cudaMemcpyAsync(y_h, y, ny, cudaMemcpyDeviceToHost, s), "D2H y")) return st;
+    if (o1d_status st = cu(cudaStreamWaitEvent(s2, e_in, 0), "wait")) return st;  // w and x are on the device
+    if (o1d_status st = o1d_backward_input(pl, dy, w, dx, s2)) return st;
+    if (o1d_status st = cu(cudaMemcpyAsync(dx_h, dx, nx, cudaMemcpyDeviceToHost, s2), "D2H dx")) return st;
+    if (o1d_status st = o1d_backward_weight(pl, x, dy, dW, ws, o1d_workspace_bytes(pl), s2)) return st;
+    if (o1d_status st = cu(cudaMemcpyAsync(dW_h, dW, nw, cudaMemcpyDeviceToHost, s2), "D2H dW")) return st;
+    if (o1d_status st = cu(cudaEventRecord(e_out, s2), "event")) return st;
+    if (o1d_status st = cu(cudaStreamWaitEvent(s, e_out, 0), "wait")) return st;
+    return cu(cudaStreamSynchronize(s), "o1d_step_host");
 }
 
 }  // extern "C"

@@ -54,6 +54,8 @@ struct o1d_plan {
     int fwd_band = 0, bi_band = 0;
     size_t ws_bytes = 0;
     o1d::SpecSet *spec = nullptr;     // null => generic kernels only
+    void *aux_stream = nullptr;       // o1d_step_host's second stream (cudaStream_t)
+    void *aux_ev[2] = {nullptr, nullptr};
     std::string describe;
 };
 
