@@ -343,6 +343,7 @@ int env_int(const char *n, int dflt) {
 struct Ctx {
     int N, C, K, Ho, Wo, BR, BC, wpg, G, nt, nsm;  // wpg: warps (bands) per tap group; G: tap groups
     bool ffma2 = false;                                  // packed fp32 FMA in the stencil
+    bool ffma2_w = false;                                // packed fp32 FMA in wgrad (measured slower: 74 vs 64 us)
     int minb = 1;                                        // __launch_bounds__ min blocks per SM (stencil)
     int gw = 2;                                          // tap groups of the wgrad kernel
     int act = 0;                                         // activation dtype (o1d_dtype)
@@ -752,6 +753,65 @@ size_t stencil_smem(const Ctx &x, const std::vector<Geo> &geo) {
 //               warp's partial of tap L in lane L; partials go to
 //               ws[plane][band][k]; the warp that completes a channel (epoch
 //               counter) sums them in f64 in (n, band) order into dW.
+// backward_weight taps of group `ds` with packed FFMA2 along block ROWS: the
+// dy values of rows (0,1), (2,3), (4,5) are register pairs (g pair, one
+// alignment for every tap), the pixel pair is the vertical pair
+// (px(i,j), px(i+1,j)) with i = r + dh, and each tap accumulates into one
+// register pair QP_d; row 6 adds into the low half.  q_d = lo + hi at the end.
+void emit_wgrad_compute_ffma2(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, const char *ind) {
+    // g pairs (rows 0..5); row 6 stays scalar
+    for (int r = 0; r < 6; r += 2)
+        for (int s = 0; s < S; ++s)
+            os << ind << "const u64 G" << r << "_" << s << " = f2pack(g" << r << "_" << s << ", g" << r + 1 << "_" << s
+               << ");\n";
+    for (int d : ds) os << ind << "u64 QP" << d << " = 0ull;\n";
+    int lo_h = 1 << 20, hi_h = -(1 << 20);
+    for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
+    std::set<std::pair<int, int>> loaded;
+    auto pxn = [](int i, int j) {
+        return std::string("px") + (i < 0 ? "m" + std::to_string(-i) : std::to_string(i)) + "_" +
+               (j < 0 ? "m" + std::to_string(-j) : std::to_string(j));
+    };
+    auto load = [&](int i, int j) {
+        if (loaded.insert({i, j}).second)
+            os << ind << "const float " << pxn(i, j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
+    };
+    for (int i = lo_h; i <= hi_h + R - 1; ++i) {
+        // pairs starting at footprint row i: taps with r = i - dh in {0, 2, 4}
+        std::vector<std::pair<int, int>> pr;  // (d, r)
+        std::vector<int> single;              // d with i - dh == 6
+        for (int d : ds) {
+            const int r = i - g.taps[d].dh;
+            if (r == 0 || r == 2 || r == 4) pr.push_back({d, r});
+            if (r == 6) single.push_back(d);
+        }
+        if (pr.empty() && single.empty()) continue;
+        std::set<int> pj;
+        for (auto &q : pr)
+            for (int s = 0; s < S; ++s) pj.insert(g.taps[q.first].dw + s);
+        for (int j : pj) load(i, j), load(i + 1, j);
+        for (int d : single)
+            for (int s = 0; s < S; ++s) load(i, g.taps[d].dw + s);
+        for (int j : pj)
+            os << ind << "const u64 PV" << (i < 0 ? "m" + std::to_string(-i) : std::to_string(i)) << "_"
+               << (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)) << " = f2pack(" << pxn(i, j) << ", "
+               << pxn(i + 1, j) << ");\n";
+        // slot-major emission: consecutive instructions hit different accumulators
+        for (int s = 0; s < S; ++s)
+            for (auto &q : pr) {
+                const int d = q.first, r = q.second, j = g.taps[d].dw + s;
+                os << ind << "QP" << d << " = ffma2(PV" << (i < 0 ? "m" + std::to_string(-i) : std::to_string(i)) << "_"
+                   << (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)) << ", G" << r << "_" << s << ", QP" << d
+                   << ");\n";
+            }
+        for (int s = 0; s < S; ++s)
+            for (int d : single)
+                os << ind << "QP" << d << " = f2pack(fmaf(" << pxn(i, g.taps[d].dw + s) << ", g6_" << s << ", f2lo(QP" << d
+                   << ")), f2hi(QP" << d << "));\n";
+    }
+    for (int d : ds) os << ind << "const float q" << d << " = f2lo(QP" << d << ") + f2hi(QP" << d << ");\n";
+}
+
 std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
                       const std::vector<int> &count) {
     std::ostringstream os;
@@ -807,7 +867,8 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  return r;\n}\n";
     const int bcg = (x.BC + 7) / 8;
     const unsigned target = (unsigned)(x.N * ncw);
-    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (ncw + 1) << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
+    os << "extern \"C\" __global__ void __launch_bounds__(" << 32 * (ncw + 1) << ", " << x.minb
+       << ") o1d_wgrad(const __grid_constant__ Params p) {\n"
        << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
        << "  float* const scr = reinterpret_cast<float*>(smem + " << off_scr << ");\n"
        << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
@@ -873,14 +934,18 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
         for (int gi = 0; gi < G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
-            for (int d : ds) os << "        float q" << d << " = 0.f;\n";
-            for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                os << "        { const float px = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
-                for (auto &u : uses)
-                    os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q"
-                       << u.first << ");";
-                os << " }\n";
-            });
+            if (x.ffma2_w) {
+                emit_wgrad_compute_ffma2(os, g, ds, "        ");
+            } else {
+                for (int d : ds) os << "        float q" << d << " = 0.f;\n";
+                for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+                    os << "        { const float px = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
+                    for (auto &u : uses)
+                        os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q"
+                           << u.first << ");";
+                    os << " }\n";
+                });
+            }
             for (size_t q = 0; q < ds.size(); ++q) os << "        v[" << q << "] = q" << ds[q] << ";\n";
             os << "      }\n";
         }
@@ -1028,6 +1093,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
+    x.ffma2_w = env_int("O1D_FFMA2_W", 0) != 0;
     x.act = d.dtype;
     if (gpc && !gpc->empty()) {
         x.home = home_tables(*gpc, sp->count, sp->nt);
