@@ -623,6 +623,13 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    int t, c, n; item_cn(item, t, c, n);\n"
        << "    const unsigned char* tile = smem + b * " << TB << ";\n"
        << "    const float* wv = wsm + b * 64;\n";
+    if (x.G > 1)  // the previous band store has long finished reading the staging area: free it now
+        os << "    if (grp == 0) {\n"
+           << "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+           << "      __syncwarp();\n"
+           << "      asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(1 + wg), \"r\"(64) : \"memory\");\n"
+           << "    }\n";
+    os << "";
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
     os << "    switch (t) {\n";
@@ -705,11 +712,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
         emit_sts(false, true);
     } else {
         // group G-1 writes first, then G-2 adds, ..., group 0 adds and stores.
-        os << "    if (grp == 0) {\n"
-           << "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
-           << "      __syncwarp();\n"
-           << "      asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(1 + wg), \"r\"(" << nb << ") : \"memory\");\n"
-           << "    }\n";
+        // ("staging free" is signalled by group 0 at the top of the iteration, see below)
         for (int gi = x.G - 1; gi >= 0; --gi) {
             os << "    if (grp == " << gi << ") {\n";
             if (gi == x.G - 1)
