@@ -402,8 +402,19 @@ int range_cost(const Geo &g, int lo, int hi) {
 // Distinct taps of tap group gi: contiguous ranges of the distinct-tap list whose
 // boundaries balance the estimated cost (groups run on different warps that
 // meet at the output combine, so the slowest group sets the pace).
+int pair_axis(const Geo &g);
+int parity_of(int v);
+bool g_parity_groups = true;  // set per plan (O1D_PARITY)
+
 std::vector<int> group_taps(const Geo &g, int gi, int G) {
     const int nd = (int)g.taps.size();
+    if (G == 2 && g_parity_groups) {  // parity of the offset along the table's pair axis
+        const int axis = pair_axis(g);
+        std::vector<int> v;
+        for (int d = 0; d < nd; ++d)
+            if (parity_of(axis == 0 ? g.taps[d].dh : g.taps[d].dw) == gi) v.push_back(d);
+        if (!v.empty() || gi == 1) return v;
+    }
     std::vector<int> cut(G + 1, 0);
     cut[G] = nd;
     for (int q = 1; q < G; ++q) cut[q] = (q * nd) / G;
@@ -546,6 +557,141 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
 //                 groups combine through the staging tile with pairwise named
 //                 barriers; group 0 warps TMA-store their own 4*7-row band.
 // No CTA-wide barrier in the steady state.
+// ---------------------------------------------------------------------------
+// Parity tap groups + packed FP32 (FFMA2) along one axis.
+//
+// With two tap groups, taps are split by the parity of their offset along the
+// table's "pair axis" (rows if the dh parities are balanced, else columns).
+// Outputs (stencil) or dy values (wgrad) are paired along that axis — rows
+// (0,1),(2,3),(4,5) + row 6, or columns likewise — so the pixel pair of every
+// FFMA2 starts at a coordinate of the group's parity: each loaded pixel sits in
+// exactly one register pair and no copies are needed.
+// ---------------------------------------------------------------------------
+int parity_of(int v) { return ((v % 2) + 2) % 2; }
+
+// 0: pair along rows (uses dh parity), 1: along columns (dw parity)
+int pair_axis(const Geo &g) {
+    int ev = 0, od = 0, ew = 0, ow = 0;
+    for (auto &t : g.taps) (parity_of(t.dh) ? od : ev)++, (parity_of(t.dw) ? ow : ew)++;
+    return std::abs(ev - od) <= std::abs(ew - ow) ? 0 : 1;
+}
+
+std::string coord(int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); }
+
+// One FMA of the paired formulation: accumulator `acc` (pair or scalar),
+// pixel (i, j) [pair: with its partner one step along the axis], tap d, and
+// the (r, s) of the output (stencil) / dy value (wgrad) it multiplies.
+struct PairOp {
+    bool pair;
+    int d, r, s, i, j;
+};
+
+// ops for taps `ds` of table g along `axis`, ordered by footprint row (liveness)
+// and slot-major within a row (independent accumulators back to back)
+std::vector<PairOp> pair_ops(const Geo &g, const std::vector<int> &ds, int axis) {
+    std::vector<PairOp> ops;
+    for (int d : ds) {
+        const int dh = g.taps[d].dh, dw = g.taps[d].dw;
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) {
+                const int u = axis == 0 ? r : s;  // coordinate along the pair axis
+                if (u == 6) ops.push_back({false, d, r, s, r + dh, s + dw});
+                else if (u % 2 == 0) ops.push_back({true, d, r, s, r + dh, s + dw});
+            }
+    }
+    std::stable_sort(ops.begin(), ops.end(), [](const PairOp &a, const PairOp &b) {
+        if (a.i != b.i) return a.i < b.i;
+        return a.r * S + a.s < b.r * S + b.s;
+    });
+    return ops;
+}
+
+// emits loads of pixel (i, j) [and the pair partner] on first use; returns the operand name
+struct PixelCache {
+    const Geo &g;
+    std::ostringstream &os;
+    const char *ind;
+    int axis;
+    std::set<std::pair<int, int>> loaded, packed;
+    std::string px(int i, int j) {
+        if (loaded.insert({i, j}).second)
+            os << ind << "const float px" << coord(i) << "_" << coord(j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0)
+               << "]);\n";
+        return "px" + coord(i) + "_" + coord(j);
+    }
+    std::string pair(int i, int j) {
+        const int i2 = axis == 0 ? i + 1 : i, j2 = axis == 0 ? j : j + 1;
+        const std::string a = px(i, j), b = px(i2, j2);
+        const std::string name = "pp" + coord(i) + "_" + coord(j);
+        if (packed.insert({i, j}).second) os << ind << "const u64 " << name << " = f2pack(" << a << ", " << b << ");\n";
+        return name;
+    }
+};
+
+// stencil: a_rs += Σ_d w_d · px(r+dh, s+dw) for the taps `ds` (assigns a_rs)
+void emit_stencil_compute_paired(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, int axis,
+                                 const char *ind) {
+    for (int d : ds) {
+        os << ind << "const float m" << d << " = ";
+        for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
+        os << ";\n" << ind << "const u64 M" << d << " = f2pack(m" << d << ", m" << d << ");\n";
+    }
+    // accumulators: pairs keyed by the first (r, s) of the pair, scalars on the last row/column
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            const int u = axis == 0 ? r : s;
+            if (u == 6) os << ind << "float AS" << r << "_" << s << " = 0.f;\n";
+            else if (u % 2 == 0) os << ind << "u64 AP" << r << "_" << s << " = 0ull;\n";
+        }
+    PixelCache pc{g, os, ind, axis, {}, {}};
+    for (const PairOp &o : pair_ops(g, ds, axis)) {
+        if (o.pair) {
+            const std::string p = pc.pair(o.i, o.j);
+            os << ind << "AP" << o.r << "_" << o.s << " = ffma2(" << p << ", M" << o.d << ", AP" << o.r << "_" << o.s << ");\n";
+        } else {
+            const std::string p = pc.px(o.i, o.j);
+            os << ind << "AS" << o.r << "_" << o.s << " = fmaf(" << p << ", m" << o.d << ", AS" << o.r << "_" << o.s << ");\n";
+        }
+    }
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            const int u = axis == 0 ? r : s;
+            if (u == 6) {
+                os << ind << "a" << r << "_" << s << " = AS" << r << "_" << s << ";\n";
+            } else if (u % 2 == 0) {
+                const int r2 = axis == 0 ? r + 1 : r, s2 = axis == 0 ? s : s + 1;
+                os << ind << "a" << r << "_" << s << " = f2lo(AP" << r << "_" << s << "); a" << r2 << "_" << s2
+                   << " = f2hi(AP" << r << "_" << s << ");\n";
+            }
+        }
+}
+
+// wgrad: q_d = Σ_{r,s} g_rs · px(r+dh, s+dw) for the taps `ds` (declares float q<d>)
+void emit_wgrad_compute_paired(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, int axis,
+                               const char *ind) {
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            const int u = axis == 0 ? r : s;
+            if (u % 2 == 0 && u < 6) {
+                const int r2 = axis == 0 ? r + 1 : r, s2 = axis == 0 ? s : s + 1;
+                os << ind << "const u64 G" << r << "_" << s << " = f2pack(g" << r << "_" << s << ", g" << r2 << "_" << s2
+                   << ");\n";
+            }
+        }
+    for (int d : ds) os << ind << "u64 QP" << d << " = 0ull; float QS" << d << " = 0.f;\n";
+    PixelCache pc{g, os, ind, axis, {}, {}};
+    for (const PairOp &o : pair_ops(g, ds, axis)) {
+        if (o.pair) {
+            const std::string p = pc.pair(o.i, o.j);
+            os << ind << "QP" << o.d << " = ffma2(" << p << ", G" << o.r << "_" << o.s << ", QP" << o.d << ");\n";
+        } else {
+            const std::string p = pc.px(o.i, o.j);
+            os << ind << "QS" << o.d << " = fmaf(" << p << ", g" << o.r << "_" << o.s << ", QS" << o.d << ");\n";
+        }
+    }
+    for (int d : ds) os << ind << "const float q" << d << " = (f2lo(QP" << d << ") + f2hi(QP" << d << ")) + QS" << d << ";\n";
+}
+
 std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::vector<int> &table_of,
                         const std::vector<int> &count) {
     std::ostringstream os;
@@ -641,7 +787,9 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
                << "{\n";
-            if (x.ffma2) {
+            if (x.ffma2 && g_parity_groups && x.G == 2) {
+                emit_stencil_compute_paired(os, g, ds, pair_axis(g), "        ");
+            } else if (x.ffma2) {
                 emit_stencil_compute_ffma2(os, g, ds, "        ");
             } else {
                 for (int r = 0; r < R; ++r)
@@ -937,7 +1085,9 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
         for (int gi = 0; gi < G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
-            if (x.ffma2_w) {
+            if (x.ffma2_w && g_parity_groups && G == 2) {
+                emit_wgrad_compute_paired(os, g, ds, pair_axis(g), "        ");
+            } else if (x.ffma2_w) {
                 emit_wgrad_compute_ffma2(os, g, ds, "        ");
             } else {
                 for (int d : ds) os << "        float q" << d << " = 0.f;\n";
@@ -1096,7 +1246,8 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
-    x.ffma2_w = env_int("O1D_FFMA2_W", 0) != 0;
+    g_parity_groups = env_int("O1D_PARITY", 0) != 0;
+    x.ffma2_w = env_int("O1D_FFMA2_W", g_parity_groups ? 1 : 0) != 0;
     x.act = d.dtype;
     if (gpc && !gpc->empty()) {
         x.home = home_tables(*gpc, sp->count, sp->nt);
