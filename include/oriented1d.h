@@ -29,8 +29,10 @@
  *   - Weights w and the weight gradient dW are fp32 [C][K] (k fastest).
  *     Activations x, y, dy, dx have the plan's dtype (fp32, bf16 or fp16);
  *     arithmetic is fp32 multiply-add with fp32 accumulation for every dtype.
- *   - A plan is immutable after creation and may be used concurrently from
- *     several host threads / streams.
+ *   - A plan is immutable after creation and may be used from several host
+ *     threads / streams concurrently (each launch of a specialised kernel takes
+ *     its own work-queue slot; up to 64 launches per pass in flight), except
+ *     o1d_step_host, which uses the plan's internal second stream.
  */
 #ifndef ORIENTED1D_H_
 #define ORIENTED1D_H_

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <set>
 #include <sstream>
@@ -218,6 +219,8 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 
 }  // namespace
 
+constexpr int kSlots = 64;  // concurrent launches per pass that can be in flight on one plan
+
 struct SpecSet {
     int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, nt = 0, nsm = 0, gw = 1;
     std::vector<Geo> fwd, bwd;  // per distinct table
@@ -228,7 +231,11 @@ struct SpecSet {
     size_t smem[3] = {0, 0, 0};
     int grid[3] = {0, 0, 0};
     int threads[3] = {0, 0, 0};
-    unsigned *d_sched = nullptr;  // 3 passes x (NT next counters + 1 done counter), then C channel counters
+    // work-queue counters: 3 passes x kSlots launch slots x (NT next counters + 1 done counter);
+    // every launch takes the next slot (host atomic), so concurrent launches on
+    // different streams never share counters; a slot is reset by its last CTA
+    unsigned *d_sched = nullptr;
+    std::atomic<unsigned> launch_seq{0};
     std::string regs[3];
 };
 
@@ -1356,7 +1363,7 @@ o1d_status spec_create(o1d_plan *pl) {
         size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
         sp->regs[i] = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
     }
-    const size_t nsched = 3 * (sp->nt + 1) + d.C;
+    const size_t nsched = (size_t)3 * kSlots * (sp->nt + 1) + d.C;
     if (cudaMalloc(&sp->d_sched, sizeof(unsigned) * nsched) != cudaSuccess ||
         cudaMemset(sp->d_sched, 0, sizeof(unsigned) * nsched) != cudaSuccess) {
         for (int j = 0; j < 3; ++j) dr.moduleUnload(sp->mod[j]);
@@ -1416,8 +1423,9 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[0] = const_cast<float *>(w);
     ptrs[1] = const_cast<void *>(b);
     ptrs[2] = ws;
-    ptrs[3] = sp->d_sched + pass * (nt + 1);
-    ptrs[4] = sp->d_sched + 3 * (nt + 1);
+    const unsigned slot = const_cast<SpecSet *>(sp)->launch_seq.fetch_add(1) % kSlots;
+    ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + slot) * (nt + 1);
+    ptrs[4] = sp->d_sched + (size_t)3 * kSlots * (nt + 1);
     ptrs[5] = dW;
     void *args[] = {blob};
     CUlaunchAttribute attr[1];

@@ -145,6 +145,28 @@ def test_errors_on_gpu():
     assert st == 6  # MISALIGNED
 
 
+def test_concurrent_streams_same_plan():
+    """One plan, launches in flight on several streams at once (work-queue slots)."""
+    wl = inputs.S1
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(8, wl.C, wl.H, wl.W, wl.K, np.array(angles), device="cuda:0")
+    xs = [torch.from_numpy(inputs.activation(plan.x_shape(), 20 + i)).cuda() for i in range(4)]
+    w = torch.from_numpy(inputs.weights(wl.C, wl.K)).cuda()
+    ref = [B.forward(plan, x, w) for x in xs]
+    refw = [B.backward_weight(plan, x, x) for x in xs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in xs]
+    outs, outw = [], []
+    for _ in range(3):
+        for x, st in zip(xs, streams):
+            with torch.cuda.stream(st):
+                outs.append(B.forward(plan, x, w, stream=st))
+                outw.append(B.backward_weight(plan, x, x, stream=st))
+    torch.cuda.synchronize()
+    for i, (y, dW) in enumerate(zip(outs, outw)):
+        assert torch.equal(y, ref[i % 4]) and torch.equal(dW, refw[i % 4])
+
+
 def test_module_autograd():
     from paper_2309_15812_b200.module import Oriented1dDWConv
     torch.manual_seed(0)
