@@ -860,7 +860,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
         os << "      }\n";
     };
     // named barriers per band (warp wg of every group): id 1+wg "free" (group 0 -> others), id 1+wpg+wg chain
-    const int nb = 32 * x.G;  // threads per named barrier
+    const int nb = 64;  // every named barrier pairs two warps (one arrives, one syncs)
     if (x.G == 1) {
         os << "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
            << "    __syncwarp();\n";
@@ -1232,7 +1232,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     const int bcg = (sp->BC + 7) / 8, brg = (sp->BR + 3) / 4;
     sp->wpg = bcg * brg;
     sp->G = env_int("O1D_G", (sp->wpg <= 2 && d.K >= 8) ? 2 : 1);  // tap groups per plane
-    if (sp->G < 1 || sp->G > 2) return false;
+    if (sp->G < 1 || sp->G > 4) return false;
     sp->nthreads = 32 * sp->wpg * sp->G;
     sp->nt = pl->n_distinct;
     sp->nsm = nsm;
@@ -1250,7 +1250,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
             if (g->pitch > 256 || g->rows > 256 || g->bytes > 100 * 1024) return false;
     }
     if (d.W > 256 || d.H > 256 || sp->nthreads > 1024) return false;
-    if (sp->BC > 8 || sp->G > 2) return false;  // one 8-block column group per band (W <= 56)
+    if (sp->BC > 8) return false;  // one 8-block column group per band (W <= 56)
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.ffma2 = env_int("O1D_FFMA2", 1) != 0;
     g_parity_groups = env_int("O1D_PARITY", 0) != 0;
