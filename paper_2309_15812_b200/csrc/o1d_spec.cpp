@@ -356,11 +356,14 @@ struct Ctx {
     int act = 0;                                         // activation dtype (o1d_dtype)
     std::vector<int> home;                               // home table per %smid (empty: TPC-pair fallback)
     bool steal = true;                                   // CTAs move to other tables once theirs is done
+    bool convert = false;                                // 16-bit tiles widened to an fp32 smem copy
     int nthreads() const { return 32 * wpg * G; }
 };
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
     os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define STEAL " << (x.steal ? 1 : 0) << "\n";
+    // tile reads: fp32 copy (convert path) or the raw activation tile
+    os << (x.convert ? "#define LDT(v) (v)\n" : "#define LDT(v) LD(v)\n");
     // activation element type in shared memory / HBM; arithmetic is fp32 throughout
     if (x.act == O1D_F32)
         os << "typedef float act_t;\n#define LD(v) (v)\n"
@@ -473,6 +476,39 @@ size_t tile_bytes_of(const std::vector<Geo> &geo) {
     return (b + 1023) & ~(size_t)1023;
 }
 
+// fp32 copy of a 16-bit tile (convert path): same pitch/rows, fp32 guard
+int guard32(const Geo &g) { return ((g.pitch * 4) + 127) & ~127; }
+size_t tile32_bytes_of(const std::vector<Geo> &geo) {
+    size_t b = 0;
+    for (auto &g : geo) b = std::max(b, (size_t)guard32(g) + (size_t)g.rows * g.pitch * 4);
+    return (b + 1023) & ~(size_t)1023;
+}
+
+// emitted by the consumer warps of a converted (16-bit) plan right after the tile
+// of ring buffer b landed: widen it to fp32 once (conflict-free sequential
+// LDS.32 -> STS.64), release the 16-bit buffer to the producer, and compute from
+// the fp32 copy with the conflict-free fp32 lane map.
+void emit_convert(std::ostringstream &os, const Ctx &x, const std::vector<Geo> &geo, size_t TB, size_t OFF32,
+                  int ncw) {
+    const int nc = 32 * ncw;
+    os << "    asm volatile(\"bar.sync 13, " << nc << ";\" ::: \"memory\");  // previous fp32 tile fully consumed\n"
+       << "    {\n      const int ctid = tid - 32;\n      switch (t) {\n";
+    for (int q = 0; q < x.nt; ++q) {
+        const Geo &g = geo[q];
+        const int npairs = g.rows * g.pitch / 2;
+        os << "      case " << q << ": {\n"
+           << "        const unsigned* src = reinterpret_cast<const unsigned*>(smem + b * " << TB << " + " << g.guard << ");\n"
+           << "        float2* dst = reinterpret_cast<float2*>(smem + " << OFF32 + guard32(g) << ");\n"
+           << "        for (int e = ctid; e < " << npairs << "; e += " << nc << ") { const unsigned v = src[e]; dst[e] = "
+           << (x.act == O1D_BF16 ? "make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));"
+                                 : "make_float2(h2f((unsigned short)(v & 0xffffu)), h2f((unsigned short)(v >> 16)));")
+           << " }\n        break;\n      }\n";
+    }
+    os << "      }\n    }\n"
+       << "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");  // 16-bit buffer free\n"
+       << "    asm volatile(\"bar.sync 13, " << nc << ";\" ::: \"memory\");  // fp32 tile complete\n";
+}
+
 size_t stage_bytes_of(const Ctx &x) {
     const int rows = ((x.BR * R + 4 * R - 1) / (4 * R)) * (4 * R);  // whole 4*7-row bands
     return ((size_t)rows * x.Wo * 4 + 1023) & ~(size_t)1023;
@@ -520,7 +556,7 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
         for (int j : pr) need.insert(j), need.insert(j + 1);
         os << ind << "{\n";
         for (int j : need)
-            os << ind << "  const float " << vname(j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
+            os << ind << "  const float " << vname(j) << " = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
         for (int j : pr) os << ind << "  const u64 " << pname(j) << " = f2pack(" << vname(j) << ", " << vname(j + 1) << ");\n";
         // emit slot-major (slot q of every (r, d) pair, then slot q+1, ...): consecutive
         // instructions update different accumulators, so no FMA waits on its predecessor
@@ -622,7 +658,7 @@ struct PixelCache {
     std::set<std::pair<int, int>> loaded, packed;
     std::string px(int i, int j) {
         if (loaded.insert({i, j}).second)
-            os << ind << "const float px" << coord(i) << "_" << coord(j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0)
+            os << ind << "const float px" << coord(i) << "_" << coord(j) << " = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0)
                << "]);\n";
         return "px" + coord(i) + "_" + coord(j);
     }
@@ -705,8 +741,9 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     emit_header(os, x, table_of, count);
     const size_t TB = tile_bytes_of(geo);
     const size_t SB = stage_bytes_of(x);
-    const size_t off_stage = 2 * TB, off_wsm = off_stage + SB, off_bar = off_wsm + 2 * 64 * 4,
-                 off_item = off_bar + 32;
+    const size_t T32 = x.convert ? tile32_bytes_of(geo) : 0, OFF32 = 2 * TB;
+    const size_t off_stage = 2 * TB + T32, off_wsm = off_stage + SB, off_bar = off_wsm + 3 * 64 * 4,
+                 off_item = off_bar + 32;  // wsm: [2] producer-staged + [1] consumer copy (convert path)
     const int ncw = x.wpg * x.G;  // consumer warps
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
     const int band = 4 * R;       // output rows per consumer warp
@@ -719,7 +756,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "  u64* const empty = full + 2;\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
-       << "  for (int i = threadIdx.x; i < 2 * " << TB / 16 << "; i += blockDim.x) {  // zero guards (and tiles)\n"
+       << "  for (int i = threadIdx.x; i < " << (2 * TB + T32) / 16 << "; i += blockDim.x) {  // zero guards (and tiles)\n"
        << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
        << "  }\n"
        << "  if (tid == 0) {\n"
@@ -774,8 +811,15 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const unsigned char* tile = smem + b * " << TB << ";\n"
-       << "    const float* wv = wsm + b * 64;\n";
+       << "    const unsigned char* tile = " << (x.convert ? "smem + " + std::to_string(OFF32) : "smem + b * " + std::to_string(TB)) << ";\n"
+       << "    const float* wv = wsm + " << (x.convert ? "128" : "b * 64") << ";\n";
+    if (x.convert) {
+        // the 16-bit buffer (and its weight slot) is released before the tap loop:
+        // keep this plane's weights in the consumer-owned slot wsm[2]
+        os << "    asm volatile(\"bar.sync 13, " << 32 * ncw << ";\" ::: \"memory\");  // previous plane's weights consumed\n"
+           << "    if (tid - 32 < " << x.K << ") wsm[128 + tid - 32] = wsm[b * 64 + tid - 32];\n";
+        emit_convert(os, x, geo, TB, OFF32, ncw);
+    }
     if (x.G > 1)  // the previous band store has long finished reading the staging area: free it now
         os << "    if (grp == 0) {\n"
            << "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
@@ -789,7 +833,8 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile + " << g.guard << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const " << (x.convert ? "float" : "act_t") << "* tb = reinterpret_cast<const " << (x.convert ? "float" : "act_t")
+           << "*>(tile + " << (x.convert ? guard32(g) : g.guard) << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < x.G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, x.G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < x.G ? "if (grp == " + std::to_string(gi) + ") " : "")
@@ -807,7 +852,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
                     os << ";\n";
                 }
                 for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                    os << "        { const float v = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
+                    os << "        { const float v = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
                     for (auto &u : uses) {
                         const int r = u.second.first, s = u.second.second;
                         os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
@@ -821,7 +866,9 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     }
     os << "    }\n"
        << "    __syncwarp();\n"
-       << "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");  // done with the tile\n";
+       << (x.convert ? std::string("")
+                     : "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" + std::to_string(32 * (ncw + 1)) +
+                           ") : \"memory\");  // done with the tile\n");
     auto store_pred = [&](int r, int s) {
         std::ostringstream q;
         if (ragged) q << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
@@ -899,7 +946,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 }
 
 size_t stencil_smem(const Ctx &x, const std::vector<Geo> &geo) {
-    return 2 * tile_bytes_of(geo) + stage_bytes_of(x) + 2 * 64 * 4 + 32 + 16;
+    return 2 * tile_bytes_of(geo) + (x.convert ? tile32_bytes_of(geo) : 0) + stage_bytes_of(x) + 3 * 64 * 4 + 32 + 16;
 }
 
 // Warp-specialised backward_weight kernel:
@@ -932,7 +979,7 @@ void emit_wgrad_compute_ffma2(std::ostringstream &os, const Geo &g, const std::v
     };
     auto load = [&](int i, int j) {
         if (loaded.insert({i, j}).second)
-            os << ind << "const float " << pxn(i, j) << " = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
+            os << ind << "const float " << pxn(i, j) << " = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
     };
     for (int i = lo_h; i <= hi_h + R - 1; ++i) {
         // pairs starting at footprint row i: taps with r = i - dh in {0, 2, 4}
@@ -981,7 +1028,8 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     const int dyrows = R * x.BR;             // padded rows, zero-filled by TMA
     const size_t DB = ((size_t)dyp * dyrows * es + 1023) & ~(size_t)1023;
     const int ncw = x.wpg * G;
-    const size_t off_dy = 2 * TB, off_scr = off_dy + 2 * DB, off_bar = off_scr + (size_t)ncw * 32 * 4,
+    const size_t T32 = x.convert ? tile32_bytes_of(geo) : 0, OFF32 = 2 * TB;
+    const size_t off_dy = 2 * TB + T32, off_scr = off_dy + 2 * DB, off_bar = off_scr + (size_t)ncw * 32 * 4,
                  off_item = off_bar + 32;
     int maxd = 0;
     std::vector<std::vector<int>> k2g(x.nt, std::vector<int>(x.K)), k2s(x.nt, std::vector<int>(x.K));
@@ -1032,7 +1080,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
-       << "  for (int i = threadIdx.x; i < 2 * " << TB / 16 << "; i += blockDim.x)  // zero guards (and tiles)\n"
+       << "  for (int i = threadIdx.x; i < " << (2 * TB + T32) / 16 << "; i += blockDim.x)  // zero guards (and tiles)\n"
        << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
        << "  if (tid == 0) { mbar_init(full, 32); mbar_init(full + 1, 32); fence_mbar_init(); }\n"
        << "  __syncthreads();\n"
@@ -1077,18 +1125,20 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "    const int item = s_item[b];\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
-       << "    const unsigned char* tile = smem + b * " << TB << ";\n"
+       << "    const unsigned char* tile = " << (x.convert ? "smem + " + std::to_string(OFF32) : "smem + b * " + std::to_string(TB)) << ";\n"
        << "    const act_t* gb = reinterpret_cast<const act_t*>(smem + " << off_dy << " + b * " << DB << ") + (" << R
        << " * br) * " << dyp << " + " << S << " * bc;\n";
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s)
             os << "    const float g" << r << "_" << s << " = active ? LD(gb[" << r * dyp + s << "]) : 0.f;\n";
+    if (x.convert) emit_convert(os, x, geo, TB, OFF32, ncw);  // also releases the dy buffer (g is in registers)
     os << "    for (int q = 0; q < " << NV << "; ++q) v[q] = 0.f;\n"
        << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
         os << "    case " << t << ": {\n"
-           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile + " << g.guard << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
+           << "      const " << (x.convert ? "float" : "act_t") << "* tb = reinterpret_cast<const " << (x.convert ? "float" : "act_t")
+           << "*>(tile + " << (x.convert ? guard32(g) : g.guard) << ") + (" << R << " * br) * " << g.pitch << " + " << S << " * bc;\n";
         for (int gi = 0; gi < G; ++gi) {
             const std::vector<int> ds = group_taps(g, gi, G);
             os << "      " << (gi ? "else " : "") << (gi + 1 < G ? "if (grp == " + std::to_string(gi) + ") " : "") << "{\n";
@@ -1099,7 +1149,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
             } else {
                 for (int d : ds) os << "        float q" << d << " = 0.f;\n";
                 for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
-                    os << "        { const float px = LD(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
+                    os << "        { const float px = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);";
                     for (auto &u : uses)
                         os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q"
                            << u.first << ");";
@@ -1112,7 +1162,9 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
         os << "      break;\n    }\n";
     }
     os << "    }\n"
-       << "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");  // tile + dy released\n"
+       << (x.convert ? std::string("")
+                     : "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" + std::to_string(32 * (ncw + 1)) +
+                           ") : \"memory\");  // tile + dy released\n")
        << "    const float part = reduce_scatter_nv(v, lane);\n"
        << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
        << "    __syncwarp();\n"
@@ -1151,7 +1203,7 @@ size_t wgrad_smem(const Ctx &x, const std::vector<Geo> &geo) {
     const size_t TB = tile_bytes_of(geo);
     const int es = x.act == O1D_F32 ? 4 : 2, vec = 16 / es;
     const size_t DB = ((size_t)((S * x.BC + vec - 1) & ~(vec - 1)) * R * x.BR * es + 1023) & ~(size_t)1023;
-    return 2 * TB + 2 * DB + (size_t)x.wpg * x.G * 32 * 4 + 32 + 16;
+    return 2 * TB + (x.convert ? tile32_bytes_of(geo) : 0) + 2 * DB + (size_t)x.wpg * x.G * 32 * 4 + 32 + 16;
 }
 
 o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH) {
@@ -1256,6 +1308,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     g_parity_groups = env_int("O1D_PARITY", 0) != 0;
     x.ffma2_w = env_int("O1D_FFMA2_W", g_parity_groups ? 1 : 0) != 0;
     x.act = d.dtype;
+    x.convert = x.act != O1D_F32 && env_int("O1D_CONVERT", 0) != 0;
     if (gpc && !gpc->empty()) {
         x.home = home_tables(*gpc, sp->count, sp->nt);
         // every table has home SMs: no stealing needed for completion
@@ -1329,6 +1382,7 @@ o1d_status spec_create(o1d_plan *pl) {
         }
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.act = d.dtype;
+    x.convert = x.act != O1D_F32 && env_int("O1D_CONVERT", 0) != 0;
     sp->smem[0] = stencil_smem(x, sp->fwd);
     sp->smem[1] = stencil_smem(x, sp->bwd);
     sp->threads[0] = sp->threads[1] = 32 * (sp->wpg * sp->G + 1);
