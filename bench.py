@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--angle", type=float, default=None,
                     help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
     ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
+    ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
+                    help="time the ConvNeXt-1D training step (images/s) instead of the layer step")
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch for --model (default 128 T / 64 B)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary bf16 measurement")
@@ -185,6 +188,76 @@ def run_reference(args):
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_model(args):
+    """ConvNeXt-1D synthetic training step (fwd + cross-entropy + bwd + AdamW), bf16
+    activations, fp32 oriented-conv weights; DDP (NCCL) over the ranks at N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_15812_b200 import convnext1d
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B = args.batch or (128 if args.model == "convnext_t_1d" else 64)
+    torch.manual_seed(0)
+    model = convnext1d.ConvNeXt1D(args.model).to(dev).to(torch.bfloat16)
+    for m in convnext1d.oriented_layers(model):
+        m.weight.data = m.weight.data.float()  # the library takes fp32 weights
+    if world > 1:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
+    opt = torch.optim.AdamW(model.parameters(), lr=1e-4)
+    g = torch.Generator(device=dev).manual_seed(rank)
+    imgs = [torch.randn(B, 3, 224, 224, device=dev, generator=g).to(torch.bfloat16) for _ in range(2)]
+    labels = [torch.randint(0, 1000, (B,), device=dev, generator=g) for _ in range(2)]
+
+    def step(i):
+        opt.zero_grad(set_to_none=True)
+        out = model(imgs[i & 1])
+        loss = torch.nn.functional.cross_entropy(out.float(), labels[i & 1])
+        loss.backward()
+        opt.step()
+        return loss
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record()
+    for i in range(args.steps):
+        loss = step(i)
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    n_or = len(convnext1d.oriented_layers(model))
+    line = {"metric": METRIC, "value": B * world / (ms * 1e-3), "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (N(0,1) images, random labels, random-init weights)",
+            "config": {"workload": f"{args.model}_train_step", "global_batch": B * world, "per_gpu_batch": B,
+                       "image": 224, "oriented_layers": n_or, "optimizer": "AdamW",
+                       "parallelism": f"ddp{world} (NCCL all-reduce of every gradient incl. dW)"},
+            "clocks": ck, "loss": float(loss.item())}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -348,6 +421,15 @@ def run_ours(args):
                                               "per_pass_frac_of_hbm")}
         except Exception as ex:  # pragma: no cover
             line["bf16"] = {"error": repr(ex)}
+    if rank == 0 and not args.no_extra and args.dtype == "f32":
+        try:
+            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--model", "convnext_t_1d", "--steps", "10",
+                                  "--warmup", "3"], capture_output=True, text=True, timeout=900,
+                                 env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
+            m = json.loads(out.stdout.strip().splitlines()[-1])
+            line["convnext_t_1d_train"] = {k: m[k] for k in ("value", "unit", "ms_per_step", "config")}
+        except Exception as ex:  # pragma: no cover
+            line["convnext_t_1d_train"] = {"error": repr(ex)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -359,6 +441,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.model:
+        return run_model(args)
     return run_ours(args)
 
 

@@ -4,6 +4,7 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 from . import binding as B
@@ -43,7 +44,8 @@ class Oriented1dDWConv(torch.nn.Module):
         self.C, self.K, self.stride = C, K, stride
         if angles_deg is None:
             angles_deg = B.direction_angles(D, C, assign, shift_deg)
-        self.register_buffer("angles_deg", torch.as_tensor(angles_deg, dtype=torch.float64), persistent=True)
+        # kept as float64 numpy (not a buffer: Module.to(dtype) must not round the angles)
+        self.angles_deg = np.asarray(angles_deg, dtype=np.float64).copy()
         self.weight = torch.nn.Parameter(torch.empty(C, K))
         torch.nn.init.uniform_(self.weight, -1.0 / math.sqrt(K), 1.0 / math.sqrt(K))
         self._plans = {}
@@ -53,7 +55,7 @@ class Oriented1dDWConv(torch.nn.Module):
         key = (N, H, W, x.dtype, x.device)
         p = self._plans.get(key)
         if p is None:
-            p = B.Plan(N, C, H, W, self.K, self.angles_deg.cpu().numpy(), stride=self.stride, dtype=x.dtype,
+            p = B.Plan(N, C, H, W, self.K, self.angles_deg, stride=self.stride, dtype=x.dtype,
                        device=x.device)
             self._plans[key] = p
         return p

@@ -174,7 +174,7 @@ def test_module_autograd():
     x = torch.randn(2, 16, 20, 20, device="cuda:0", requires_grad=True)
     y = m(x)
     y.square().sum().backward()
-    angles = m.angles_deg.cpu().numpy().tolist()
+    angles = m.angles_deg.tolist()
     oh, ow = T.taps_table(7, 3, angles)
     oh, ow = np.array(oh), np.array(ow)
     xd = x.detach().double().cpu().numpy()
@@ -199,3 +199,20 @@ def test_step_host_matches_device_path():
     assert torch.equal(y, B.forward(plan, xd, wd).cpu())
     assert torch.equal(dx, B.backward_input(plan, dyd, wd).cpu())
     assert torch.equal(dW, B.backward_weight(plan, xd, dyd).cpu())
+
+
+def test_convnext1d_harness_trains():
+    """The ConvNeXt-T-1D harness runs a bf16 training step through liboriented1d
+    (smaller image; every oriented layer's weight receives a finite gradient)."""
+    from paper_2309_15812_b200 import convnext1d
+    torch.manual_seed(0)
+    m = convnext1d.ConvNeXt1D("convnext_t_1d", num_classes=10).cuda().to(torch.bfloat16)
+    for layer in convnext1d.oriented_layers(m):
+        layer.weight.data = layer.weight.data.float()
+    x = torch.randn(2, 3, 64, 64, device="cuda:0").to(torch.bfloat16)
+    out = m(x)
+    loss = torch.nn.functional.cross_entropy(out.float(), torch.tensor([1, 3], device="cuda:0"))
+    loss.backward()
+    assert torch.isfinite(loss)
+    for layer in convnext1d.oriented_layers(m):
+        assert layer.weight.grad is not None and torch.isfinite(layer.weight.grad).all()
