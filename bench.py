@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--angle", type=float, default=None,
                     help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
     ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
+    ap.add_argument("--K", type=int, default=None, help="kernel length (experiments; default: the workload's 31)")
     ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
                     help="time the ConvNeXt-1D training step (images/s) instead of the layer step")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch for --model (default 128 T / 64 B)")
@@ -280,6 +281,9 @@ def run_ours(args):
     if args.dirs is not None:
         from dataclasses import replace
         wl = replace(wl, D=args.dirs)
+    if args.K is not None:
+        from dataclasses import replace
+        wl = replace(wl, K=args.K)
     angles = B.direction_angles(wl.D, wl.C, wl.assign)
     if args.angle is not None:
         angles = np.full(wl.C, float(args.angle))

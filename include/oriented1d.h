@@ -170,6 +170,12 @@ O1D_API void o1d_plan_destroy(o1d_plan *plan);
  * problem is served by the generic kernels. */
 O1D_API o1d_status o1d_spec_source(const o1d_desc *d, const double *angles_deg, int32_t pass, char *buf,
                                    size_t *len);
+/* Diagnostics: with O1D_TRACE=1 in the environment at plan creation, the
+ * specialised kernels append (globaltimer ns, tag) u64 pairs to a plan-owned
+ * device buffer (first u64 = record count; tag = kind:4 | warp:4 | smid:8 |
+ * block:16 | item:32).  Synchronises the device, copies up to `bytes` into
+ * `host` and clears the buffer.  Returns the bytes copied (0: tracing off). */
+O1D_API size_t o1d_debug_trace(const o1d_plan *plan, void *host, size_t bytes);
 O1D_API const char *o1d_last_error(void);
 O1D_API const char *o1d_version(void);
 

@@ -29,7 +29,8 @@ ASSIGN = {"contiguous": 0, "cycled": 1}
 EXPORTS = ["o1d_make_taps", "o1d_direction_angles", "o1d_plan_create", "o1d_plan_out_shape",
            "o1d_plan_get_taps", "o1d_plan_describe", "o1d_workspace_bytes", "o1d_forward",
            "o1d_backward_input", "o1d_backward_weight", "o1d_step_host_workspace_bytes", "o1d_step_host",
-           "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source"]
+           "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source",
+           "o1d_debug_trace"]
 
 
 class O1DError(RuntimeError):
@@ -73,6 +74,7 @@ def lib():
                 "o1d_plan_destroy": (None, [vp]),
                 "o1d_last_error": (ctypes.c_char_p, []),
                 "o1d_version": (ctypes.c_char_p, []),
+                "o1d_debug_trace": (ctypes.c_size_t, [vp, vp, ctypes.c_size_t]),
                 "o1d_spec_source": (st, [ctypes.POINTER(_Desc), f64p, i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
             }
             for name, (res, args) in sig.items():
@@ -170,6 +172,15 @@ class Plan:
         ow = np.empty((self.C, self.K), np.int16)
         _check(lib().o1d_plan_get_taps(self._h, _ptr(oh), _ptr(ow)))
         return oh, ow
+
+    def debug_trace(self) -> np.ndarray:
+        """O1D_TRACE event records since the last call: uint64 [n, 2] (time ns, tag); empty if tracing is off."""
+        buf = np.zeros(1 + 2 * (1 << 21), np.uint64)
+        got = lib().o1d_debug_trace(self._h, buf.ctypes.data, buf.nbytes)
+        if not got:
+            return np.zeros((0, 2), np.uint64)
+        rec = buf[1:].reshape(-1, 2)
+        return rec[rec[:, 0] != 0]
 
     def workspace_bytes(self) -> int:
         return int(lib().o1d_workspace_bytes(self._h))

@@ -167,6 +167,11 @@ static o1d_status plan_host_init(const o1d_desc *d, const double *angles_deg, o1
     return O1D_OK;
 }
 
+size_t o1d_debug_trace(const o1d_plan *pl, void *host, size_t bytes) {
+    if (!pl || !host) return 0;
+    return spec_trace(pl, host, bytes);
+}
+
 o1d_status o1d_spec_source(const o1d_desc *d, const double *angles_deg, int32_t pass, char *buf, size_t *len) {
     if (!len) return fail(O1D_INVALID_ARG, "o1d_spec_source: NULL len");
     o1d_plan pl;

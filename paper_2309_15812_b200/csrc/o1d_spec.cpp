@@ -220,9 +220,13 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 }  // namespace
 
 constexpr int kSlots = 64;  // concurrent launches per pass that can be in flight on one plan
+constexpr size_t kTraceBytes = 8 + ((size_t)32 << 20);  // count + 2^21 (time, tag) records
 
 struct SpecSet {
     int BR = 0, BC = 0, nthreads = 0, wpg = 0, G = 1, nt = 0, nsm = 0, gw = 1;
+    bool v2 = false;                      // any pass on the v2 pipeline (one tap group, NS-slot ring, shared zero rows)
+    bool v2p[3] = {false, false, false};  // per pass
+    int pitch2[3] = {0, 0, 0}, rows2[3] = {0, 0, 0}, ns2 = 0;
     std::vector<Geo> fwd, bwd;  // per distinct table
     std::vector<int> count;     // planes per table
     CUmodule mod[3] = {nullptr, nullptr, nullptr};
@@ -235,6 +239,7 @@ struct SpecSet {
     // every launch takes the next slot (host atomic), so concurrent launches on
     // different streams never share counters; a slot is reset by its last CTA
     unsigned *d_sched = nullptr;
+    unsigned long long *d_trace = nullptr;  // diagnostics (O1D_TRACE=1): event records of the next launches
     std::atomic<unsigned> launch_seq{0};
     std::string regs[3];
 };
@@ -255,6 +260,8 @@ struct Params {
   unsigned* sched;   // [NT] next-plane counters, [NT] = done counter
   unsigned* cnt;     // [C] per-channel epoch counters (wgrad)
   float* dW;
+  int only;          // >= 0: this launch processes table `only` alone (table-sequential mode)
+  u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
 };
 __device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
@@ -290,6 +297,17 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) { u64 d; asm("fma.rn.f
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ u32 smid() { u32 r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+__device__ __forceinline__ u64 gtimer() { u64 r; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(r)); return r; }
+// diagnostics: one (time, tag) record in this warp's private region (256 records
+// per warp, no atomics); tag = kind:4 | warp:4 | smid:8 | block:16 | item:32
+__device__ __forceinline__ void trace_ev(u64* tr, u32 kind, int item, int& n) {
+  if (!tr) return;
+  const u64 i = ((u64)blockIdx.x * 32 + (threadIdx.x >> 5)) * 256 + (n++ & 255);
+  if (i >= (1ull << 21)) return;
+  tr[1 + 2 * i] = gtimer();
+  tr[2 + 2 * i] = ((u64)kind << 60) | ((u64)((threadIdx.x >> 5) & 15) << 56) | ((u64)(smid() & 255) << 48) |
+                  ((u64)(blockIdx.x & 0xffff) << 32) | (u32)item;
+}
 // 32 values per lane -> lane L returns the warp sum of v[L] (31 shuffles)
 __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 #pragma unroll
@@ -309,10 +327,10 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 // specialised code path in the instruction cache) and moves on to the next
 // table when it is exhausted.  `raw` is a counter value fetched one plane
 // ahead, so the atomic's latency is hidden behind a whole plane of compute.
-__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried) {
+__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried, bool steal) {
   while (tcur >= 0) {
     if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
-    if (++tried >= NT || !STEAL) { tcur = -1; break; }
+    if (++tried >= NT || !STEAL || !steal) { tcur = -1; break; }
     tcur = tcur + 1 == NT ? 0 : tcur + 1;
     raw = atomicAdd(sched + tcur, 1u);
   }
@@ -324,8 +342,16 @@ __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsign
 __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   t = item >> 22;
   const int i = item & 0x3FFFFF;
+#if CMAJOR
+  // consecutive items walk the table's channels first: the planes in flight on the GPU
+  // form a compact address range (n-major walks stride C*H*W apart)
+  const int nch = CHOFF[t + 1] - CHOFF[t];
+  n = i / nch;
+  c = CHLIST[CHOFF[t] + (i - n * nch)];
+#else
   c = CHLIST[CHOFF[t] + i / NB];
   n = i - (i / NB) * NB;
+#endif
 }
 __device__ __forceinline__ void sched_exit(unsigned* sched) {
   __threadfence();
@@ -357,11 +383,13 @@ struct Ctx {
     std::vector<int> home;                               // home table per %smid (empty: TPC-pair fallback)
     bool steal = true;                                   // CTAs move to other tables once theirs is done
     bool convert = false;                                // 16-bit tiles widened to an fp32 smem copy
+    bool v2 = false;                                     // v2 pipeline (see gen_stencil2)
     int nthreads() const { return 32 * wpg * G; }
 };
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
-    os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define STEAL " << (x.steal ? 1 : 0) << "\n";
+    os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define STEAL " << (x.steal ? 1 : 0) << "\n"
+       << "#define CMAJOR " << env_int("O1D_CMAJOR", 1) << "\n";
     // tile reads: fp32 copy (convert path) or the raw activation tile
     os << (x.convert ? "#define LDT(v) (v)\n" : "#define LDT(v) LD(v)\n");
     // activation element type in shared memory / HBM; arithmetic is fp32 throughout
@@ -470,6 +498,29 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
     }
 }
 
+// I-cache warm-up chunks (v2): the straight-line tap code of a table is split into
+// g_chunks guarded chunks `if (wm & bit) { ... }`; a real item runs them all
+// (wm = ~0), the warm-up pass at kernel start runs one chunk per consumer warp so
+// the cold code is fetched by all warps in parallel (measured: the first tap loop
+// of a table otherwise takes ~10 us of instruction fetch instead of ~1.6 us).
+int g_chunks = 0;
+struct Chunker {
+    std::ostringstream &os;
+    const char *ind;
+    int total, n, cur = -1;
+    void at(int idx) {
+        if (n <= 1 || total <= 0) return;
+        const int k = (int)((long)idx * n / total);
+        if (k == cur) return;
+        if (cur >= 0) os << ind << "}\n";
+        os << ind << "if (wm & " << (1u << k) << "u) {\n";
+        cur = k;
+    }
+    void end() {
+        if (n > 1 && cur >= 0) os << ind << "}\n";
+    }
+};
+
 size_t tile_bytes_of(const std::vector<Geo> &geo) {
     size_t b = 0;
     for (auto &g : geo) b = std::max(b, (size_t)g.guard + g.bytes);
@@ -535,12 +586,19 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
     for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
     auto vname = [](int j) { return std::string("v") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
     auto pname = [](int j) { return std::string("P") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
+    int nrows = 0;
+    for (int i = lo_h; i <= hi_h + R - 1; ++i)
+        for (int r = 0; r < R; ++r)
+            if (std::any_of(ds.begin(), ds.end(), [&](int d) { return g.taps[d].dh == i - r; })) { ++nrows; break; }
+    Chunker ch{os, ind, nrows, g_chunks};
+    int row_idx = 0;
     for (int i = lo_h; i <= hi_h + R - 1; ++i) {
         std::vector<std::pair<int, int>> pairs;  // (r, d)
         for (int r = 0; r < R; ++r)
             for (int d : ds)
                 if (g.taps[d].dh == i - r) pairs.push_back({r, d});
         if (pairs.empty()) continue;
+        ch.at(row_idx++);
         std::set<int> scal, pr;
         for (auto &p : pairs) {
             const int dw = g.taps[p.second].dw;
@@ -581,6 +639,7 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
             }
         os << ind << "}\n";
     }
+    ch.end();
     for (int r = 0; r < R; ++r) {
         os << ind << "a" << r << "_0 = f2lo(A" << r << "_0) + B" << r << "_0;\n"
            << ind << "a" << r << "_1 = f2hi(A" << r << "_0) + f2lo(B" << r << "_1);\n"
@@ -756,6 +815,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "  u64* const empty = full + 2;\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  int trn = 0;\n"
        << "  for (int i = threadIdx.x; i < " << (2 * TB + T32) / 16 << "; i += blockDim.x) {  // zero guards (and tiles)\n"
        << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
        << "  }\n"
@@ -768,18 +828,19 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    // ------------------------------------------------------------ producer\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      // buffer b is free once every consumer warp released item it-2: a named\n"
        << "      // barrier per buffer parity (the producer blocks in hardware, no spinning)\n"
        << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
        << "      int item = -1;\n"
-       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
+       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried, p.only < 0); sched_prefetch(p.sched, tcur, raw); }\n"
        << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
        << "      int t2 = 0, c2 = 0, n2 = 0;\n"
        << "      if (item >= 0) item_cn(item, t2, c2, n2);\n"
        << "      if (lane == 0 && item >= 0) {   // issue the tile load first: it is the long pole\n"
+       << "        trace_ev(p.trace, 1, item, trn);\n"
        << "        unsigned char* dst = smem + b * " << TB << ";\n"
        << "        switch (t2) {\n";
     for (int t = 0; t < x.nt; ++t)
@@ -807,8 +868,10 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     if (bcg != 1) os << "  // (several warps per band: bands are stored by the warp with wg % bcg == 0)\n";
     os << "  for (int it = 0;; ++it) {\n"
        << "    const int b = it & 1;\n"
+       << "    if (lane == 0) trace_ev(p.trace, 2, it, trn);\n"
        << "    mbar_wait(full + b, (it >> 1) & 1);\n"
        << "    const int item = s_item[b];\n"
+       << "    if (lane == 0) trace_ev(p.trace, 3, item, trn);\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
        << "    const unsigned char* tile = " << (x.convert ? "smem + " + std::to_string(OFF32) : "smem + b * " + std::to_string(TB)) << ";\n"
@@ -866,6 +929,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
     }
     os << "    }\n"
        << "    __syncwarp();\n"
+       << "    if (lane == 0) trace_ev(p.trace, 4, item, trn);\n"
        << (x.convert ? std::string("")
                      : "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" + std::to_string(32 * (ncw + 1)) +
                            ") : \"memory\");  // done with the tile\n");
@@ -939,9 +1003,364 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "        asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
        << "      }\n"
        << "    }\n"
+       << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
        << "  }\n"
        << "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
        << "}\n";
+    return os.str();
+}
+
+// ===========================================================================
+// v2 pipeline (default): one tap group per warp, one persistent CTA per SM.
+//
+// Measured on the v1 design (tools/trace_pass.py, O1D_TRACE): with the taps
+// split over two warp groups, the per-plane group combine (pairwise named
+// barriers + a second partial pass through shared memory) took ~30% of every
+// consumer warp's time; with one group the warps computed ~2x faster per FMA
+// but waited for tiles most of the time (a 2-slot ring = one plane of
+// lookahead), and the v1 wgrad's per-plane reductions stalled the same way.
+//
+// v2: one CTA per SM = a producer warp + P consumer "pairs" (wpg warps each,
+// one band of 4 block rows per warp, ALL taps).  Items (planes) go round-robin
+// to the pairs (item it -> pair it % P) and to an NS-slot ring (slot it % NS),
+// so NS - P planes are in flight while P are computed.  A slot holds only the
+// image rows (TMA box from row 0, OOB columns zero-filled by the TMA unit);
+// consecutive slots share zero rows that serve as the vertical halo (reading
+// R1), so a slot is ~35% smaller than a v1 tile with its halo.  Stencil
+// outputs are staged in the consumed slot; the PRODUCER issues the TMA store
+// (consumers never wait for it) before it reloads the slot.  backward_weight
+// also TMA-loads the dy plane into a per-pair slot that the pair releases as
+// soon as its dy block is in registers.
+// ---------------------------------------------------------------------------
+struct Lay2 {
+    int NS = 3, P = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
+    size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
+           total = 0;
+    int ncw() const { return P * wpg; }
+    size_t slot(int s) const { return off_t + zb + (size_t)s * (zb + tb); }
+};
+
+Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad) {
+    Lay2 L;
+    L.wpg = x.wpg;
+    L.hin = Hin;
+    L.P = std::max(1, std::min(8, env_int("O1D_P", std::max(1, 8 / x.wpg))));
+    while (L.P * L.wpg > 15) --L.P;
+    for (auto &g : geo) {
+        L.pitch = std::max(L.pitch, g.pitch);
+        L.zrows = std::max(L.zrows, std::max(-g.minDH, R * x.BR - Hin + g.maxDH) + 1);
+    }
+    L.zb = ((size_t)L.zrows * L.pitch * es + 127) & ~(size_t)127;
+    L.tb = ((size_t)Hin * L.pitch * es + 127) & ~(size_t)127;
+    if (wgrad) {
+        const int vec = 16 / es;
+        L.dyp = (S * x.BC + vec - 1) & ~(vec - 1);
+        L.dyrows = R * x.BR;
+        L.db = ((size_t)L.dyp * L.dyrows * es + 127) & ~(size_t)127;
+    }
+    // header: full[NSmax], empty[NSmax], dyempty[8] mbarriers | s_item | weights | scratch | dy slots | zero rows + slots
+    const int NSmax = 16;
+    L.off_item = 8 * (2 * (size_t)NSmax + 8);
+    L.off_w = (L.off_item + 4 * (size_t)NSmax + 15) & ~(size_t)15;
+    L.off_scr = L.off_w + (wgrad ? 0 : (size_t)NSmax * 64 * 4);
+    L.off_stg = (L.off_scr + (wgrad ? (size_t)L.ncw() * 32 * 4 : 0) + 127) & ~(size_t)127;
+    L.sb = wgrad ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
+    L.off_dy = L.off_stg + (size_t)L.ncw() * L.sb;
+    L.off_t = (L.off_dy + (size_t)L.P * L.db + 1023) & ~(size_t)1023;
+    const size_t budget = (size_t)env_int("O1D_SMEM_KB", 220) * 1024;
+    const int fit = budget > L.off_t + L.zb ? (int)((budget - L.off_t - L.zb) / (L.zb + L.tb)) : 0;
+    L.NS = std::min(std::min(fit, NSmax), env_int("O1D_NS", 3 * L.P));
+    L.total = L.off_t + (size_t)L.NS * (L.zb + L.tb) + L.zb;
+    return L;
+}
+
+// geometry as the v2 emitters see it: tile row 0 = image row 0, uniform pitch
+std::vector<Geo> geo2(const std::vector<Geo> &geo, const Lay2 &L) {
+    std::vector<Geo> v = geo;
+    for (auto &g : v) g.minDH = 0, g.x0 = 0, g.pitch = L.pitch;
+    return v;
+}
+
+void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool wgrad) {
+    os << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
+       << "  u64* const full = reinterpret_cast<u64*>(smem);\n"
+       << "  u64* const empty = full + 16;\n"
+       << "  u64* const dyempty = full + 32;\n"
+       << "  int* const s_item = reinterpret_cast<int*>(smem + " << L.off_item << ");\n"
+       << "  float* const wsm = reinterpret_cast<float*>(smem + " << L.off_w << ");\n"
+       << "  unsigned char* const tiles = smem + " << L.off_t << ";\n"
+       << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  int trn = 0;\n"
+       << "  for (int i = tid; i < " << (L.total - L.off_t) / 16 << "; i += " << nthreads << ")  // zero rows + slots\n"
+       << "    reinterpret_cast<uint4*>(tiles)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int s = 0; s < " << L.NS << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << L.wpg << "); }\n";
+    if (wgrad) os << "    for (int q = 0; q < " << L.P << "; ++q) mbar_init(dyempty + q, " << L.wpg << ");\n";
+    os << "    fence_mbar_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n";
+}
+
+// producer warp.  Item it goes to slot it % NS (reused once the pair that had
+// item it - NS released it) and pair it % P; after the scheduler runs dry,
+// P end markers (-1) are published so every pair stops.
+void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool wgrad, int es) {
+    const int NS = L.NS, P = L.P;
+    const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0);  // exact box bytes
+    os << "  if (warp == 0) {\n"
+       << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
+       << "    pdl_wait();\n"
+       << "    unsigned base = 0;   // the first NS items are grabbed with one atomic (fills the ring without round trips)\n"
+       << "    if (lane == 0) {\n"
+       << "      trace_ev(p.trace, 0, -1, trn);\n"
+       << "      tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n"
+       << "      base = atomicAdd(p.sched + tcur, " << NS << "u);\n"
+       << "      raw = atomicAdd(p.sched + tcur, 1u);\n"
+       << "    }\n"
+       << "    int ends = 0;\n"
+       << "    for (int it = 0;; ++it) {\n"
+       << "      const int s = it % " << NS << ";\n"
+       << "      if (it >= " << NS << ") mbar_wait(empty + s, ((it / " << NS << ") & 1) ^ 1);   // pair done with item it - NS\n"
+       << "      int item = -1;\n"
+       << "      if (lane == 0 && ends == 0) {\n"
+       << "        if (it < " << NS << " && base + it < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(base + it);\n"
+       << "        else { item = sched_resolve(p.sched, tcur, raw, tried, p.only < 0); sched_prefetch(p.sched, tcur, raw); }\n"
+       << "      }\n"
+       << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
+       << "      int t2 = 0, c2 = 0, n2 = 0;\n"
+       << "      if (item >= 0) item_cn(item, t2, c2, n2);\n";
+    if (wgrad)  // the pair's dy slot is free once it copied the dy block of item it - P
+        os << "      if (item >= 0 && it >= " << P << ") mbar_wait(dyempty + it % " << P << ", ((it / " << P << ") & 1) ^ 1);\n";
+    os << "      if (lane == 0) {\n"
+       << "        s_item[s] = item;\n"
+       << "        if (item >= 0) {\n"
+       << "          trace_ev(p.trace, 1, item, trn);\n"
+       << "          mbar_expect_tx(full + s, " << bytes << "u);\n"
+       << "          tma_load(tiles + " << L.zb << " + s * " << L.zb + L.tb << ", &p.in_map[0], 0, 0, c2, n2, full + s);\n";
+    if (wgrad)
+        os << "          tma_load(smem + " << L.off_dy << " + (it % " << P << ") * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s);\n";
+    os << "        }\n"
+       << "      }\n";
+    if (!wgrad)
+        os << "      if (item >= 0)\n"
+           << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
+    os << "      mbar_arrive(full + s);   // 32 producer arrivals (+ the bytes) complete the phase\n"
+       << "      if (item < 0 && ++ends == " << P << ") break;\n"
+       << "    }\n"
+       << "    pdl_trigger();\n"
+       << "    if (lane == 0) sched_exit(p.sched);\n"
+       << "    return;\n"
+       << "  }\n"
+       << "  const int cw = warp - 1, q = cw / " << L.wpg << ", wg = cw - q * " << L.wpg << ";\n"
+       << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
+       << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
+       << "  if (!active) { bc = 0; br = 0; }\n";
+}
+
+// consumer item-loop head (v2): it < 0 is the I-cache warm-up pass over the CTA's
+// home table (one code chunk per warp, on whatever the slot holds; results dropped)
+#define V2_LOOP_HEAD \
+    "    const bool warm = it < 0;\n" \
+    "    const int s = warm ? 0 : it % " << L.NS << ";\n" \
+    "    int item = 0, t = 0, c = 0, n = 0;\n" \
+    "    unsigned wm = 0xffffffffu;\n" \
+    "    if (warm) {\n" \
+    "      t = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n" \
+    "      wm = " << (g_chunks > 1 ? "1u << (cw % " + std::to_string(g_chunks) + ")" : std::string("0xffffffffu")) << ";\n" \
+    "    } else {\n" \
+    "      if (lane == 0) trace_ev(p.trace, 2, it, trn);\n" \
+    "      mbar_wait(full + s, (it / " << L.NS << ") & 1);\n" \
+    "      item = s_item[s];\n" \
+    "      if (lane == 0) trace_ev(p.trace, 3, item, trn);\n" \
+    "      if (item < 0) break;\n" \
+    "      item_cn(item, t, c, n);\n" \
+    "    }\n"
+
+std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
+                         const std::vector<int> &count, int Hin, const Lay2 &L) {
+    std::ostringstream os;
+    emit_header(os, x, table_of, count);
+    const std::vector<Geo> geo = geo2(geo_in, L);
+    const int nthreads = 32 * (L.ncw() + 1);
+    g_chunks = env_int("O1D_WARM", 1) ? std::min(32, L.ncw()) : 0;
+    const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
+    const int es = x.act == O1D_F32 ? 4 : 2;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_stencil(const __grid_constant__ Params p) {\n";
+    emit_v2_prologue(os, L, nthreads, false);
+    emit_v2_producer(os, x, L, false, es);
+    os << "  // -------------------------------------------------------------- consumers\n"
+       << "  unsigned char* const stg = smem + " << L.off_stg << " + cw * " << L.sb << ";   // this warp's output band\n"
+       << "  const int row0 = " << 4 * R << " * wg;\n"
+       << "  for (int it = q - " << L.P << ";; it += " << L.P << ") {\n"
+       << V2_LOOP_HEAD
+       << "    unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
+       << "    const float* wv = wsm + s * 64;\n";
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
+    os << "    switch (t) {\n";
+    for (int t = 0; t < x.nt; ++t) {
+        const Geo &g = geo[t];
+        os << "    case " << t << ": {\n"
+           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile) + (" << R << " * br) * " << L.pitch << " + " << S
+           << " * bc;\n";
+        const std::vector<int> ds = group_taps(g, 0, 1);
+        if (x.ffma2) {
+            emit_stencil_compute_ffma2(os, g, ds, "      ");
+        } else {
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) os << "      a" << r << "_" << s << " = 0.f;\n";
+            for (int d : ds) {
+                os << "      const float m" << d << " = ";
+                for (size_t k = 0; k < g.taps[d].ks.size(); ++k) os << (k ? " + " : "") << "wv[" << g.taps[d].ks[k] << "]";
+                os << ";\n";
+            }
+            for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+                os << "      { const float v = LD(tb[" << i * L.pitch + j << "]);";
+                for (auto &u : uses) {
+                    const int r = u.second.first, s = u.second.second;
+                    os << " a" << r << "_" << s << " = fmaf(v, m" << u.first << ", a" << r << "_" << s << ");";
+                }
+                os << " }\n";
+            });
+        }
+        os << "      break;\n    }\n";
+    }
+    os << "    }\n"
+       << "    if (warm) continue;\n"
+       << "    __syncwarp();\n"
+       << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n"
+       << "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n"
+       << "    __syncwarp();\n"
+       << "    if (active) {\n"
+       << "      act_t* const sto = reinterpret_cast<act_t*>(stg) + (" << R << " * br - row0) * " << x.Wo << " + " << S << " * bc;\n";
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            os << "      ";
+            if (ragged) os << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
+            os << "sto[" << r * x.Wo + s << "] = to_act(a" << r << "_" << s << ");\n";
+        }
+    os << "    }\n"
+       << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+       << "    __syncwarp();\n"
+       << "    if (lane == 0 && row0 < " << x.Ho << ") {\n"
+       << "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
+       << "                   :: \"l\"(&p.out_map), \"r\"(sa(stg)), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n) : \"memory\");\n"
+       << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+       << "    }\n"
+       << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+       << "  }\n"
+       << "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
+       << "}\n";
+    g_chunks = 0;
+    return os.str();
+}
+
+// backward_weight, v2: x tiles through the slot ring, dy planes through one slot
+// per pair (released right after the pair copied its dy blocks to registers).
+std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
+                       const std::vector<int> &count, int Hin, const Lay2 &L) {
+    std::ostringstream os;
+    emit_header(os, x, table_of, count);
+    const std::vector<Geo> geo = geo2(geo_in, L);
+    const int nthreads = 32 * (L.ncw() + 1);
+    g_chunks = env_int("O1D_WARM", 1) ? std::min(32, L.ncw()) : 0;
+    const int es = x.act == O1D_F32 ? 4 : 2;
+    int maxd = 0;
+    for (int t = 0; t < x.nt; ++t) maxd = std::max(maxd, (int)geo[t].taps.size());
+    int NV = 1;
+    while (NV < maxd) NV *= 2;  // reduce-scatter width (<= 32 distinct taps)
+    os << "__constant__ unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
+    for (int t = 0; t < x.nt; ++t) {
+        os << (t ? "," : "") << "{";
+        for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << geo[t].k2d[k];
+        os << "}";
+    }
+    os << "};\n"
+       << "__device__ __forceinline__ float reduce_scatter_nv(float (&v)[" << NV << "], int lane) {\n"
+       << "#pragma unroll\n"
+       << "  for (int s = " << NV / 2 << "; s >= 1; s >>= 1) {\n"
+       << "    const bool up = lane & s;\n"
+       << "#pragma unroll\n"
+       << "    for (int i = 0; i < s; ++i) {\n"
+       << "      const float send = up ? v[i] : v[i + s];\n"
+       << "      const float keep = up ? v[i + s] : v[i];\n"
+       << "      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);\n"
+       << "    }\n  }\n"
+       << "  float r = v[0];\n"
+       << "#pragma unroll\n"
+       << "  for (int s = " << NV << "; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);\n"
+       << "  return r;\n}\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_wgrad(const __grid_constant__ Params p) {\n";
+    emit_v2_prologue(os, L, nthreads, true);
+    emit_v2_producer(os, x, L, true, es);
+    os << "  float* const scr = reinterpret_cast<float*>(smem + " << L.off_scr << ");\n"
+       << "  const act_t* const dys = reinterpret_cast<const act_t*>(smem + " << L.off_dy << " + q * " << L.db << ") + (" << R
+       << " * br) * " << L.dyp << " + " << S << " * bc;\n"
+       << "  float v[" << NV << "];\n"
+       << "  for (int it = q - " << L.P << ";; it += " << L.P << ") {\n"
+       << V2_LOOP_HEAD;
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s)
+            os << "    const float g" << r << "_" << s << " = active ? LD(dys[" << r * L.dyp + s << "]) : 0.f;\n";
+    os << "    __syncwarp();\n"
+       << "    if (lane == 0 && !warm) mbar_arrive(dyempty + q);   // dy block in registers: the pair's dy slot is free\n"
+       << "    const unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
+       << "    for (int k = 0; k < " << NV << "; ++k) v[k] = 0.f;\n"
+       << "    switch (t) {\n";
+    for (int t = 0; t < x.nt; ++t) {
+        const Geo &g = geo[t];
+        os << "    case " << t << ": {\n"
+           << "      const act_t* tb = reinterpret_cast<const act_t*>(tile) + (" << R << " * br) * " << L.pitch << " + " << S
+           << " * bc;\n";
+        const std::vector<int> ds = group_taps(g, 0, 1);
+        for (int d : ds) os << "      float q" << d << " = 0.f;\n";
+        int npx = 0, ipx = 0;
+        for_each_pixel(g, ds, [&](int, int, const std::vector<std::pair<int, std::pair<int, int>>> &) { ++npx; });
+        Chunker ch{os, "      ", npx, g_chunks};
+        for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+            ch.at(ipx++);
+            os << "      { const float px = LD(tb[" << i * L.pitch + j << "]);";
+            for (auto &u : uses)
+                os << " q" << u.first << " = fmaf(g" << u.second.first << "_" << u.second.second << ", px, q" << u.first << ");";
+            os << " }\n";
+        });
+        ch.end();
+        for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] = q" << ds[k] << ";\n";
+        os << "      break;\n    }\n";
+    }
+    os << "    }\n"
+       << "    if (warm) continue;\n"
+       << "    __syncwarp();\n"
+       << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }  // x slot released\n"
+       << "    const float part = reduce_scatter_nv(v, lane);\n"
+       << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
+       << "    __syncwarp();\n"
+       << "    float* wsp = p.ws + ((u64)(c * " << x.N << " + n) * " << L.wpg << " + wg) * " << x.K << ";\n"
+       << "    for (int k = lane; k < " << x.K << "; k += 32) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
+       << "    __syncwarp();\n"
+       << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+       << "  }\n"
+       << "}\n";
+    const int NE = x.N * L.wpg;
+    os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
+       << "  __shared__ double part[8][64];\n"
+       << "  pdl_wait();\n"
+       << "  const int c = blockIdx.x, j = threadIdx.x >> 5 /* 0..7 */, lane = threadIdx.x & 31;\n"
+       << "  const float* base = ws + (u64)c * " << NE << " * " << x.K << ";\n"
+       << "  for (int k = lane; k < " << x.K << "; k += 32) {\n"
+       << "    double s = 0.0;\n"
+       << "#pragma unroll 16\n"
+       << "    for (int e = j; e < " << NE << "; e += 8) s += (double)__ldcg(base + (u64)e * " << x.K << " + k);\n"
+       << "    part[j][k] = s;\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  if (threadIdx.x < " << x.K << ") {\n"
+       << "    double s = 0.0;\n"
+       << "    for (int k = 0; k < 8; ++k) s += part[k][threadIdx.x];\n"
+       << "    dW[c * " << x.K << " + threadIdx.x] = (float)s;\n"
+       << "  }\n"
+       << "}\n";
+    g_chunks = 0;
     return os.str();
 }
 
@@ -1080,6 +1499,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  u64* const full = reinterpret_cast<u64*>(smem + " << off_bar << ");\n"
        << "  int* const s_item = reinterpret_cast<int*>(smem + " << off_item << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  int trn = 0;\n"
        << "  for (int i = threadIdx.x; i < " << (2 * TB + T32) / 16 << "; i += blockDim.x)  // zero guards (and tiles)\n"
        << "    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
        << "  if (tid == 0) { mbar_init(full, 32); mbar_init(full + 1, 32); fence_mbar_init(); }\n"
@@ -1087,17 +1507,18 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { tcur = HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
        << "      int item = -1;\n"
-       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried); sched_prefetch(p.sched, tcur, raw); }\n"
+       << "      if (lane == 0) { item = sched_resolve(p.sched, tcur, raw, tried, p.only < 0); sched_prefetch(p.sched, tcur, raw); }\n"
        << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
        << "      if (lane == 0) {\n"
        << "        s_item[b] = item;\n"
        << "        if (item >= 0) {\n"
        << "          int t2, c2, n2; item_cn(item, t2, c2, n2);\n"
+       << "          trace_ev(p.trace, 1, item, trn);\n"
        << "          unsigned char* dst = smem + b * " << TB << ";\n"
        << "          switch (t2) {\n";
     for (int t = 0; t < x.nt; ++t)
@@ -1121,8 +1542,10 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  float v[" << NV << "];\n"
        << "  for (int it = 0;; ++it) {\n"
        << "    const int b = it & 1;\n"
+       << "    if (lane == 0) trace_ev(p.trace, 2, it, trn);\n"
        << "    mbar_wait(full + b, (it >> 1) & 1);\n"
        << "    const int item = s_item[b];\n"
+       << "    if (lane == 0) trace_ev(p.trace, 3, item, trn);\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n);\n"
        << "    const unsigned char* tile = " << (x.convert ? "smem + " + std::to_string(OFF32) : "smem + b * " + std::to_string(TB)) << ";\n"
@@ -1165,12 +1588,14 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << (x.convert ? std::string("")
                      : "    asm volatile(\"bar.arrive %0, %1;\" :: \"r\"(14 + b), \"r\"(" + std::to_string(32 * (ncw + 1)) +
                            ") : \"memory\");  // tile + dy released\n")
+       << "    if (lane == 0) trace_ev(p.trace, 4, item, trn);\n"
        << "    const float part = reduce_scatter_nv(v, lane);\n"
        << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
        << "    __syncwarp();\n"
        << "    float* wsp = p.ws + ((u64)(c * " << x.N << " + n) * " << x.wpg << " + wg) * " << x.K << ";\n"
        << "    for (int k = lane; k < " << x.K << "; k += 32)\n"
        << "      if (K2G[t][k] == grp) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
+       << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
        << "  }\n"
        << "}\n";
     // finalize (second launch; the kernel boundary orders the partial writes):
@@ -1259,6 +1684,7 @@ std::vector<int> home_tables(const std::vector<int> &gpc_of_smid, const std::vec
     }
     std::vector<int> ordered;
     for (auto &g : groups) ordered.insert(ordered.end(), g.second.begin(), g.second.end());
+    if (env_int("O1D_HOME_REV", 0)) std::reverse(ordered.begin(), ordered.end());  // experiment: SM order reversed
     long acc = 0;
     int t = 0;
     const int m = (int)ordered.size();
@@ -1310,7 +1736,13 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     x.act = d.dtype;
     x.convert = x.act != O1D_F32 && env_int("O1D_CONVERT", 0) != 0;
     if (gpc && !gpc->empty()) {
-        x.home = home_tables(*gpc, sp->count, sp->nt);
+        // SMs per table in proportion to the table's work: planes x estimated issue cost per 7x7
+        // block (FMA instructions + footprint loads; measured: cheap 45/135-degree tables otherwise
+        // finish early and their SMs idle through the tail)
+        std::vector<int> work(sp->nt);
+        for (int t = 0; t < sp->nt; ++t)
+            work[t] = sp->count[t] * (env_int("O1D_COSTW", 1) ? range_cost(sp->fwd[t], 0, (int)sp->fwd[t].taps.size()) + 100 : 1);
+        x.home = home_tables(*gpc, work, sp->nt);
         // every table has home SMs: no stealing needed for completion
         std::vector<int> seen(sp->nt, 0);
         for (int h : x.home) seen[h] = 1;
@@ -1327,15 +1759,36 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
             for (int gi = 0; gi < x.gw; ++gi) maxd = std::max(maxd, (int)group_taps(g, gi, x.gw).size());
         if (maxd > 32) return false;
     }
+    std::vector<int> table_of(pl->table_of.begin(), pl->table_of.end());
+    // v2 pipeline per pass (O1D_V2 bit mask: 1 forward + backward_input, 2 backward_weight)
+    const int mask = x.convert ? 0 : env_int("O1D_V2", 3);
+    int maxd_all = 0;
+    for (auto &g : sp->fwd) maxd_all = std::max(maxd_all, (int)g.taps.size());
+    const int hin[3] = {d.H, pl->P, d.H};
+    for (int i = 0; i < 3; ++i) {
+        const Lay2 L = lay2(x, i == 1 ? sp->bwd : sp->fwd, es, hin[i], i == 2);
+        const bool want = (mask >> (i == 2 ? 1 : 0)) & 1;
+        sp->v2p[i] = want && sp->BC <= 8 && (i < 2 || maxd_all <= 32) && L.NS >= L.P + 1 && L.total + 16 <= 227 * 1024;
+        if (sp->v2p[i]) {
+            Ctx xi = x;
+            xi.G = 1;
+            sp->pitch2[i] = L.pitch;
+            sp->rows2[i] = hin[i];
+            sp->ns2 = L.NS;
+            src[i] = i < 2 ? gen_stencil2(xi, i == 0 ? sp->fwd : sp->bwd, table_of, sp->count, hin[i], L)
+                           : gen_wgrad2(xi, sp->fwd, table_of, sp->count, hin[i], L);
+        }
+    }
+    sp->v2 = sp->v2p[0] || sp->v2p[1] || sp->v2p[2];
     Ctx xw = x;
     xw.G = x.gw;
-    for (const std::vector<Geo> *g : {&sp->fwd, &sp->bwd})
-        if (stencil_smem(x, *g) > 220 * 1024) return false;
-    if (wgrad_smem(xw, sp->fwd) > 220 * 1024) return false;
-    std::vector<int> table_of(pl->table_of.begin(), pl->table_of.end());
-    src[0] = gen_stencil(x, sp->fwd, table_of, sp->count);
-    src[1] = gen_stencil(x, sp->bwd, table_of, sp->count);
-    src[2] = gen_wgrad(xw, sp->fwd, table_of, sp->count);
+    for (int i = 0; i < 2; ++i)
+        if (!sp->v2p[i] && stencil_smem(x, i == 0 ? sp->fwd : sp->bwd) > 220 * 1024) return false;
+    if (!sp->v2p[2] && wgrad_smem(xw, sp->fwd) > 220 * 1024) return false;
+    if (!sp->v2p[0]) src[0] = gen_stencil(x, sp->fwd, table_of, sp->count);
+    if (!sp->v2p[1]) src[1] = gen_stencil(x, sp->bwd, table_of, sp->count);
+    if (!sp->v2p[2]) src[2] = gen_wgrad(xw, sp->fwd, table_of, sp->count);
+    if (sp->v2p[0]) sp->G = 1, sp->nthreads = 32 * lay2(x, sp->fwd, es, d.H, false).ncw();
     sp->gw = x.gw;
     return true;
 }
@@ -1383,13 +1836,26 @@ o1d_status spec_create(o1d_plan *pl) {
     Ctx x{d.N, d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->wpg, sp->G, sp->nt, nsm};
     x.act = d.dtype;
     x.convert = x.act != O1D_F32 && env_int("O1D_CONVERT", 0) != 0;
-    sp->smem[0] = stencil_smem(x, sp->fwd);
-    sp->smem[1] = stencil_smem(x, sp->bwd);
-    sp->threads[0] = sp->threads[1] = 32 * (sp->wpg * sp->G + 1);
-    Ctx xw = x;
-    xw.G = sp->gw;
-    sp->threads[2] = 32 * (sp->wpg * sp->gw + 1);
-    sp->smem[2] = wgrad_smem(xw, sp->fwd);
+    {
+        const int es = (int)dtype_size(d.dtype);
+        const Lay2 L[3] = {lay2(x, sp->fwd, es, d.H, false), lay2(x, sp->bwd, es, pl->P, false),
+                           lay2(x, sp->fwd, es, d.H, true)};
+        Ctx x1 = x;
+        x1.G = env_int("O1D_G", (sp->wpg <= 2 && d.K >= 8) ? 2 : 1);
+        Ctx xw = x;
+        xw.G = sp->gw;
+        for (int i = 0; i < 3; ++i) {
+            if (sp->v2p[i]) {
+                sp->smem[i] = L[i].total + 16, sp->threads[i] = 32 * (L[i].ncw() + 1);
+            } else if (i < 2) {
+                sp->smem[i] = stencil_smem(x1, i == 0 ? sp->fwd : sp->bwd);
+                sp->threads[i] = 32 * (sp->wpg * x1.G + 1);
+            } else {
+                sp->threads[2] = 32 * (sp->wpg * sp->gw + 1);
+                sp->smem[2] = wgrad_smem(xw, sp->fwd);
+            }
+        }
+    }
     const char *fnames[3] = {"o1d_stencil", "o1d_stencil", "o1d_wgrad"};
     PFN_cuOccupancyMaxActiveBlocksPerMultiprocessor_v6050 occ = nullptr;
     std::string e;
@@ -1424,12 +1890,14 @@ o1d_status spec_create(o1d_plan *pl) {
         delete sp;
         return fail(O1D_CUDA_ERROR, "scheduler counter allocation failed");
     }
+    if (env_flag("O1D_TRACE") && cudaMalloc(&sp->d_trace, kTraceBytes) == cudaSuccess)
+        cudaMemset(sp->d_trace, 0, kTraceBytes);
     pl->spec = sp;
     char buf[768];
     snprintf(buf, sizeof buf,
-             "spec(persistent warp-specialised, 7x7 blocks, %d consumer threads/CTA (%d tap groups), %d tap tables, TMA 4-D double-buffered; "
+             "spec%s(persistent warp-specialised, 7x7 blocks, %d consumer threads/CTA (%d tap groups), %d tap tables, TMA 4-D %d-slot ring; "
              "fwd grid %d smem %zu [%s]; bwd_in grid %d [%s]; wgrad grid %d smem %zu [%s])",
-             sp->nthreads, sp->G, sp->nt, sp->grid[0], sp->smem[0], sp->regs[0].c_str(), sp->grid[1], sp->regs[1].c_str(),
+             sp->v2 ? "-v2" : "", sp->nthreads, sp->G, sp->nt, sp->v2 ? sp->ns2 : 2, sp->grid[0], sp->smem[0], sp->regs[0].c_str(), sp->grid[1], sp->regs[1].c_str(),
              sp->grid[2], sp->smem[2], sp->regs[2].c_str());
     pl->describe = buf;
     if (env_flag("O1D_VERBOSE")) fprintf(stderr, "[o1d] %s\n", buf);
@@ -1442,6 +1910,7 @@ void spec_destroy(o1d_plan *pl) {
     for (int i = 0; i < 3; ++i)
         if (sp->mod[i]) drv().moduleUnload(sp->mod[i]);
     if (sp->d_sched) cudaFree(sp->d_sched);
+    if (sp->d_trace) cudaFree(sp->d_trace);
     delete sp;
     pl->spec = nullptr;
 }
@@ -1458,13 +1927,16 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const int nt = sp->nt;
-    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 6 * sizeof(void *)];
+    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 8 * sizeof(void *)];
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(blob);
     const std::vector<Geo> &geo = pass == 1 ? sp->bwd : sp->fwd;
     // input maps (x for forward / wgrad, dy for backward_input), one box per table
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
-    for (int t = 0; t < nt; ++t)
-        if (o1d_status st = encode(&maps[t], a, d.dtype, inW, inH, d.C, d.N, geo[t].pitch, geo[t].rows)) return st;
+    for (int t = 0; t < nt; ++t) {
+        // v2: one box for every table (uniform pitch, image rows only); v1: the table's own footprint
+        const int bw = sp->v2p[pass] ? sp->pitch2[pass] : geo[t].pitch, bh = sp->v2p[pass] ? sp->rows2[pass] : geo[t].rows;
+        if (o1d_status st = encode(&maps[t], a, d.dtype, inW, inH, d.C, d.N, bw, bh)) return st;
+    }
     if (pass != 2) {  // dense output band box for the TMA store
         const int oW = pass == 1 ? d.W : pl->Q, oH = pass == 1 ? d.H : pl->P;
         if (o1d_status st = encode(&maps[nt], b, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
@@ -1481,6 +1953,9 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + slot) * (nt + 1);
     ptrs[4] = sp->d_sched + (size_t)3 * kSlots * (nt + 1);
     ptrs[5] = dW;
+    int *only = reinterpret_cast<int *>(ptrs + 6);
+    *only = -1;
+    ptrs[7] = sp->d_trace;
     void *args[] = {blob};
     CUlaunchAttribute attr[1];
     attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -1495,7 +1970,18 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     cfg.hStream = static_cast<CUstream>(stream);
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    CUresult r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
+    CUresult r = CUDA_SUCCESS;
+    if (env_int("O1D_SEQ", 0) != 0 && nt > 1) {
+        // table-sequential: one launch per distinct table, the whole GPU on one code path at a time
+        for (int t = 0; t < nt && r == CUDA_SUCCESS; ++t) {
+            *only = t;
+            const unsigned sl = const_cast<SpecSet *>(sp)->launch_seq.fetch_add(1) % kSlots;
+            ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + sl) * (nt + 1);
+            r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
+        }
+    } else {
+        r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
+    }
     if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of specialised kernel: " + cu_err(r));
     if (pass == 2) {
         const void *wsp = ws;
@@ -1508,6 +1994,16 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
         if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of wgrad finalize: " + cu_err(r));
     }
     return O1D_OK;
+}
+
+size_t spec_trace(const o1d_plan *pl, void *host, size_t bytes) {
+    const SpecSet *sp = pl->spec;
+    if (!sp || !sp->d_trace) return 0;
+    const size_t n = std::min(bytes, kTraceBytes);
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(host, sp->d_trace, n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    cudaMemset(sp->d_trace, 0, kTraceBytes);
+    return n;
 }
 
 o1d_status spec_source(const o1d_plan *pl, int pass, std::string *out) {

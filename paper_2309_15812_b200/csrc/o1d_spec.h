@@ -14,6 +14,8 @@ void spec_destroy(o1d_plan *pl);
 bool spec_has(const o1d_plan *pl, int pass);
 int spec_launches(const o1d_plan *pl, int pass);
 size_t spec_workspace_bytes(const o1d_plan *pl);
+// diagnostics: copy (and reset) the O1D_TRACE event buffer; returns bytes copied (0: tracing off)
+size_t spec_trace(const o1d_plan *pl, void *host, size_t bytes);
 // pass 0: a=x, w, b=y; pass 1: a=dy, w, b=dx; pass 2: a=x, b=dy, dW, ws
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW,
                     float *ws, void *stream);
