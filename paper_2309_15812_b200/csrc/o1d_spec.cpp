@@ -283,6 +283,20 @@ __device__ __forceinline__ void mbar_wait(u64* b, u32 ph) {
   asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra W_%=;\n}\n"
                :: "r"(sa(b)), "r"(ph), "r"(0x100000u) : "memory");
 }
+// streaming TMA load: the tile is read once, so it is marked evict-first in L2 (the
+// kernel's code, constants and scheduler counters then stay L2-resident across launches)
+__device__ __forceinline__ u64 policy_evict_first() {
+  u64 p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p;
+}
+__device__ __forceinline__ void tma_load_ef(void* dst, const TmaDesc* m, int x, int y, int z, int w, u64* b, u64 pol) {
+  if (!pol) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 :: "r"(sa(dst)), "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(sa(b)) : "memory");
+    return;
+  }
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+               :: "r"(sa(dst)), "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(sa(b)), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tma_load(void* dst, const TmaDesc* m, int x, int y, int z, int w, u64* b) {
   asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
                :: "r"(sa(dst)), "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(sa(b)) : "memory");
@@ -504,6 +518,7 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
 // the cold code is fetched by all warps in parallel (measured: the first tap loop
 // of a table otherwise takes ~10 us of instruction fetch instead of ~1.6 us).
 int g_chunks = 0;
+#define EFH (env_int("O1D_EF", 1) != 0)  // evict-first L2 hints on the streaming TMA traffic (v2)
 struct Chunker {
     std::ostringstream &os;
     const char *ind;
@@ -584,60 +599,79 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
            << "_0 = 0.f;\n";
     int lo_h = 1 << 20, hi_h = -(1 << 20);
     for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
-    auto vname = [](int j) { return std::string("v") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
-    auto pname = [](int j) { return std::string("P") + (j < 0 ? "m" + std::to_string(-j) : std::to_string(j)); };
-    int nrows = 0;
-    for (int i = lo_h; i <= hi_h + R - 1; ++i)
-        for (int r = 0; r < R; ++r)
-            if (std::any_of(ds.begin(), ds.end(), [&](int d) { return g.taps[d].dh == i - r; })) { ++nrows; break; }
-    Chunker ch{os, ind, nrows, g_chunks};
-    int row_idx = 0;
+    // rows of the block footprint: (i, (r, d) uses, pixels to load, even-aligned pairs)
+    struct Row {
+        int i;
+        std::vector<std::pair<int, int>> pairs;
+        std::set<int> need, pr;
+    };
+    std::vector<Row> rows;
     for (int i = lo_h; i <= hi_h + R - 1; ++i) {
-        std::vector<std::pair<int, int>> pairs;  // (r, d)
+        Row rw{i, {}, {}, {}};
         for (int r = 0; r < R; ++r)
             for (int d : ds)
-                if (g.taps[d].dh == i - r) pairs.push_back({r, d});
-        if (pairs.empty()) continue;
-        ch.at(row_idx++);
-        std::set<int> scal, pr;
-        for (auto &p : pairs) {
+                if (g.taps[d].dh == i - r) rw.pairs.push_back({r, d});
+        if (rw.pairs.empty()) continue;
+        std::set<int> scal;
+        for (auto &p : rw.pairs) {
             const int dw = g.taps[p.second].dw;
             if (((dw % 2) + 2) % 2 == 0) {
-                for (int s = 0; s < 6; s += 2) pr.insert(dw + s);
+                for (int s = 0; s < 6; s += 2) rw.pr.insert(dw + s);
                 scal.insert(dw + 6);
             } else {
-                for (int s = 1; s < 7; s += 2) pr.insert(dw + s);
+                for (int s = 1; s < 7; s += 2) rw.pr.insert(dw + s);
                 scal.insert(dw);
             }
         }
-        std::set<int> need(scal);
-        for (int j : pr) need.insert(j), need.insert(j + 1);
-        os << ind << "{\n";
-        for (int j : need)
-            os << ind << "  const float " << vname(j) << " = LDT(tb[" << (i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
-        for (int j : pr) os << ind << "  const u64 " << pname(j) << " = f2pack(" << vname(j) << ", " << vname(j + 1) << ");\n";
+        rw.need = scal;
+        for (int j : rw.pr) rw.need.insert(j), rw.need.insert(j + 1);
+        rows.push_back(rw);
+    }
+    auto cn = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    auto vname = [&](int i, int j) { return "v" + cn(i) + "_" + cn(j); };
+    auto pname = [&](int i, int j) { return "P" + cn(i) + "_" + cn(j); };
+    // loads of footprint row k are emitted LA rows ahead of its FMAs (software pipelining:
+    // with two consumer warps per SM sub-partition the LDS latency is otherwise exposed)
+    // (the look-ahead stays inside one warm-up chunk: values never cross a chunk guard)
+    const int LA = std::max(0, env_int("O1D_LA", 1));
+    auto loads = [&](const Row &rw) {
+        for (int j : rw.need)
+            os << ind << "const float " << vname(rw.i, j) << " = LDT(tb[" << (rw.i - g.minDH) * g.pitch + (j - g.x0) << "]);\n";
+        for (int j : rw.pr)
+            os << ind << "const u64 " << pname(rw.i, j) << " = f2pack(" << vname(rw.i, j) << ", " << vname(rw.i, j + 1) << ");\n";
+    };
+    const int nrows = (int)rows.size();
+    auto chunk_of = [&](int k) { return g_chunks > 1 ? (int)((long)k * g_chunks / nrows) : 0; };
+    Chunker ch{os, ind, nrows, g_chunks};
+    for (int k = 0; k < nrows; ++k) {
+        ch.at(k);
+        const bool first = k == 0 || chunk_of(k - 1) != chunk_of(k);
+        if (first)  // chunk start: this row and the look-ahead rows of the chunk
+            for (int k2 = k; k2 <= k + LA && k2 < nrows && chunk_of(k2) == chunk_of(k); ++k2) loads(rows[k2]);
+        else if (k + LA < nrows && chunk_of(k + LA) == chunk_of(k))
+            loads(rows[k + LA]);
+        const Row &rw = rows[k];
         // emit slot-major (slot q of every (r, d) pair, then slot q+1, ...): consecutive
         // instructions update different accumulators, so no FMA waits on its predecessor
         for (int q = 0; q < 4; ++q)
-            for (auto &p : pairs) {
+            for (auto &p : rw.pairs) {
                 const int r = p.first, d = p.second, dw = g.taps[d].dw;
                 if (((dw % 2) + 2) % 2 == 0) {
                     if (q < 3) {
                         const int s = 2 * q;
-                        os << ind << "  A" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
+                        os << ind << "A" << r << "_" << s << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
                     } else {
-                        os << ind << "  A" << r << "_6 = fmaf(" << vname(dw + 6) << ", m" << d << ", A" << r << "_6);\n";
+                        os << ind << "A" << r << "_6 = fmaf(" << vname(rw.i, dw + 6) << ", m" << d << ", A" << r << "_6);\n";
                     }
                 } else {
                     if (q < 3) {
                         const int s = 2 * q + 1;
-                        os << ind << "  B" << r << "_" << s << " = ffma2(" << pname(dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
+                        os << ind << "B" << r << "_" << s << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
                     } else {
-                        os << ind << "  B" << r << "_0 = fmaf(" << vname(dw) << ", m" << d << ", B" << r << "_0);\n";
+                        os << ind << "B" << r << "_0 = fmaf(" << vname(rw.i, dw) << ", m" << d << ", B" << r << "_0);\n";
                     }
                 }
             }
-        os << ind << "}\n";
     }
     ch.end();
     for (int r = 0; r < R; ++r) {
@@ -1110,6 +1144,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     os << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
+       << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
        << "    unsigned base = 0;   // the first NS items are grabbed with one atomic (fills the ring without round trips)\n"
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
@@ -1136,9 +1171,9 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "        if (item >= 0) {\n"
        << "          trace_ev(p.trace, 1, item, trn);\n"
        << "          mbar_expect_tx(full + s, " << bytes << "u);\n"
-       << "          tma_load(tiles + " << L.zb << " + s * " << L.zb + L.tb << ", &p.in_map[0], 0, 0, c2, n2, full + s);\n";
+       << "          tma_load_ef(tiles + " << L.zb << " + s * " << L.zb + L.tb << ", &p.in_map[0], 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
     if (wgrad)
-        os << "          tma_load(smem + " << L.off_dy << " + (it % " << P << ") * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s);\n";
+        os << "          tma_load_ef(smem + " << L.off_dy << " + (it % " << P << ") * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
     os << "        }\n"
        << "      }\n";
     if (!wgrad)
@@ -1182,7 +1217,9 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     emit_header(os, x, table_of, count);
     const std::vector<Geo> geo = geo2(geo_in, L);
     const int nthreads = 32 * (L.ncw() + 1);
-    g_chunks = env_int("O1D_WARM", 1) ? std::min(32, L.ncw()) : 0;
+    // O1D_WARM bit 1: chunked I-cache warm-up for the stencils.  Off by default: with the
+    // evict-first TMA traffic the code stays L2-resident and the chunk guards cost ~9% issue
+    g_chunks = (env_int("O1D_WARM", 2) & 1) ? std::min(32, L.ncw()) : 0;
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
     const int es = x.act == O1D_F32 ? 4 : 2;
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_stencil(const __grid_constant__ Params p) {\n";
@@ -1243,8 +1280,10 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
        << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0 && row0 < " << x.Ho << ") {\n"
-       << "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
-       << "                   :: \"l\"(&p.out_map), \"r\"(sa(stg)), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n) : \"memory\");\n"
+       << (EFH ? "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;\"\n"
+                 "                   :: \"l\"(&p.out_map), \"r\"(sa(stg)), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n), \"l\"(policy_evict_first()) : \"memory\");\n"
+               : "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
+                 "                   :: \"l\"(&p.out_map), \"r\"(sa(stg)), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n) : \"memory\");\n")
        << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
        << "    }\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
@@ -1263,7 +1302,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     emit_header(os, x, table_of, count);
     const std::vector<Geo> geo = geo2(geo_in, L);
     const int nthreads = 32 * (L.ncw() + 1);
-    g_chunks = env_int("O1D_WARM", 1) ? std::min(32, L.ncw()) : 0;
+    g_chunks = (env_int("O1D_WARM", 2) & 2) ? std::min(32, L.ncw()) : 0;  // bit 2: wgrad warm-up (measured: on)
     const int es = x.act == O1D_F32 ? 4 : 2;
     int maxd = 0;
     for (int t = 0; t < x.nt; ++t) maxd = std::max(maxd, (int)geo[t].taps.size());
