@@ -1219,7 +1219,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     const int nthreads = 32 * (L.ncw() + 1);
     // O1D_WARM bit 1: chunked I-cache warm-up for the stencils.  Off by default: with the
     // evict-first TMA traffic the code stays L2-resident and the chunk guards cost ~9% issue
-    g_chunks = (env_int("O1D_WARM", 2) & 1) ? std::min(32, L.ncw()) : 0;
+    g_chunks = (env_int("O1D_WARM", 0) & 1) ? std::min(32, L.ncw()) : 0;
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
     const int es = x.act == O1D_F32 ? 4 : 2;
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_stencil(const __grid_constant__ Params p) {\n";
@@ -1294,6 +1294,231 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     return os.str();
 }
 
+// backward_weight taps with packed FP32 (v2).  Taps adjacent along the table's
+// run axis (axis 0: same dh, dw and dw-1; axis 1: same dw, dh and dh-1) share
+// the pixel: for pixel px and dy values g(u), g(u+1) one step apart along that
+// axis, q[tap a] += g(u) px and q[tap a-1] += g(u+1) px is one fma.rn.f32x2 with
+// px as the broadcast operand and (g(u), g(u+1)) an aligned dy register pair
+// (u even).  Which tap pair that is depends on the pixel's parity along the
+// axis, so each tap has two accumulator halves (set E for even pixel
+// coordinates, set O for odd), summed at the end; uses without a partner are
+// scalar FMAs into the tap's half of the matching set.
+void emit_wgrad_compute_runs(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, int axis,
+                             const char *ind, int chunks) {
+    auto cn = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    std::map<std::pair<int, int>, int> at;  // (dh, dw) -> distinct tap
+    for (int d : ds) at[{g.taps[d].dh, g.taps[d].dw}] = d;
+    auto A = [&](int d) { return axis == 0 ? g.taps[d].dw : g.taps[d].dh; };
+    auto Bc = [&](int d) { return axis == 0 ? g.taps[d].dh : g.taps[d].dw; };
+    auto tap_at = [&](int b, int a) {  // tap with pair-axis coordinate a, other b
+        auto it = at.find(axis == 0 ? std::make_pair(b, a) : std::make_pair(a, b));
+        return it == at.end() ? -1 : it->second;
+    };
+    auto par = [](int v) { return ((v % 2) + 2) % 2; };
+    // accumulators: set P (0 = E, 1 = O) pair keyed by its lo tap (coordinate a with par(a) == P)
+    // and hi tap (a - 1); a tap whose partner is absent keeps a scalar.
+    auto acc_of = [&](int P, int d, bool *is_pair, bool *is_lo, int *lo_tap) {
+        const int a = A(d), b = Bc(d);
+        const int lo = par(a) == P ? d : tap_at(b, a + 1);
+        const int hi = par(a) == P ? tap_at(b, a - 1) : d;
+        *is_pair = lo >= 0 && hi >= 0;
+        *is_lo = lo == d;
+        *lo_tap = lo >= 0 ? lo : d;
+        return std::string(*is_pair ? "QP" : "QS") + std::to_string(P) + "_" + std::to_string(*is_pair ? lo : d);
+    };
+    // lone uses of a paired accumulator: a separate scalar per tap (O1D_WG_LONE=1) or
+    // the pair half (=0)
+    const bool lone_sep = env_int("O1D_WG_LONE", 1) != 0;
+    if (lone_sep)
+        for (int d : ds) os << ind << "float QL" << d << " = 0.f;\n";
+    // declarations
+    std::set<std::string> decl;
+    for (int P = 0; P < 2; ++P)
+        for (int d : ds) {
+            bool ip, il;
+            int lt;
+            const std::string n = acc_of(P, d, &ip, &il, &lt);
+            if (decl.insert(n).second) os << ind << (ip ? "u64 " : "float ") << n << (ip ? " = 0ull;\n" : " = 0.f;\n");
+        }
+    // dy register pairs along the axis: (g(u), g(u+1)) for even u in 0..5
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            const int u = axis == 0 ? s : r;
+            if (u % 2 == 0 && u < 6) {
+                const int r2 = axis == 0 ? r : r + 1, s2 = axis == 0 ? s + 1 : s;
+                os << ind << "const u64 GP" << r << "_" << s << " = f2pack(g" << r << "_" << s << ", g" << r2 << "_" << s2 << ");\n";
+            }
+        }
+    int npx = 0, ipx = 0;
+    for_each_pixel(g, ds, [&](int, int, const std::vector<std::pair<int, std::pair<int, int>>> &) { ++npx; });
+    Chunker ch{os, ind, npx, chunks};
+    for_each_pixel(g, ds, [&](int i, int j, const std::vector<std::pair<int, std::pair<int, int>>> &uses) {
+        ch.at(ipx++);
+        os << ind << "{ const float px = LD(tb[" << i * g.pitch + j << "]); const u64 PX = f2pack(px, px);";
+        const int P = par(axis == 0 ? j : i);
+        // uses keyed by (other block coordinate, coordinate along the axis)
+        std::map<std::pair<int, int>, int> u2d;
+        for (auto &u : uses) {
+            const int r = u.second.first, s = u.second.second;
+            u2d[axis == 0 ? std::make_pair(r, s) : std::make_pair(s, r)] = u.first;
+        }
+        std::set<std::pair<int, int>> done;
+        for (auto &kv : u2d) {
+            const int o = kv.first.first, uu = kv.first.second, d = kv.second;
+            if (done.count(kv.first)) continue;
+            const int r = axis == 0 ? o : uu, s = axis == 0 ? uu : o;
+            auto nx = u2d.find({o, uu + 1});
+            bool ip, il;
+            int lt;
+            const std::string acc = acc_of(P, d, &ip, &il, &lt);
+            if (uu % 2 == 0 && uu < 6 && nx != u2d.end() && ip && il) {
+                // lo: tap d (coordinate a = pixel - u), hi: tap at a - 1 == the tap of use u + 1
+                os << " " << acc << " = ffma2(GP" << r << "_" << s << ", PX, " << acc << ");";
+                done.insert(kv.first);
+                done.insert(nx->first);
+            } else {
+                done.insert(kv.first);
+                if (ip && lone_sep) {
+                    os << " QL" << d << " = fmaf(g" << r << "_" << s << ", px, QL" << d << ");";
+                } else if (ip) {
+                    os << " " << acc << " = " << (il ? "f2pack(fmaf(g" : "f2pack(f2lo(" + acc + "), fmaf(g") << r << "_" << s
+                       << ", px, " << (il ? "f2lo(" : "f2hi(") << acc << "))" << (il ? ", f2hi(" + acc + "));" : "));");
+                } else {
+                    os << " " << acc << " = fmaf(g" << r << "_" << s << ", px, " << acc << ");";
+                }
+            }
+        }
+        os << " }\n";
+    });
+    ch.end();
+    for (int d : ds) {
+        std::string term[2];
+        for (int P = 0; P < 2; ++P) {
+            bool ip, il;
+            int lt;
+            const std::string n = acc_of(P, d, &ip, &il, &lt);
+            term[P] = ip ? (il ? "f2lo(" + n + ")" : "f2hi(" + n + ")") : n;
+        }
+        os << ind << "const float q" << d << " = " << term[0] << " + " << term[1] << (lone_sep ? " + QL" + std::to_string(d) : std::string()) << ";\n";
+    }
+    (void)cn;
+}
+
+// backward_weight taps with packed FP32, pixel pairs (v2, default).  Mirror of the
+// stencil's A/B scheme: the dy value g(r,s) is the broadcast operand (a plain
+// register), the pixel pair (p(u), p(u+1)) one step apart along the table's run
+// axis is an aligned register pair (u even, block-relative: every pixel sits in
+// exactly one pair, loaded with two LDS.32, no copies), and the accumulator pair
+// holds two taps adjacent along that axis: (q[d], q[d + step]).  A tap is the
+// low half of one pair and the high half of another (its partners on either
+// side), so both are summed at the end; uses with no partner are scalar FMAs.
+void emit_wgrad_compute_pp(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, int sh, int sw,
+                           const char *ind, int chunks) {
+    // (sh, sw): pair step = tap displacement of the two halves; the low pixel of a pair is the
+    // one with an even column (sw != 0) or an even row (sw == 0): a partition of the pixels
+    auto cn = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    auto par = [](int v) { return ((v % 2) + 2) % 2; };
+    auto is_lo = [&](int i, int j) { return sw != 0 ? par(j) == 0 : par(i) == 0; };
+    std::map<std::pair<int, int>, int> at;  // (dh, dw) -> distinct tap
+    for (int d : ds) at[{g.taps[d].dh, g.taps[d].dw}] = d;
+    auto next_of = [&](int d) {
+        auto it = at.find({g.taps[d].dh + sh, g.taps[d].dw + sw});
+        return it == at.end() ? -1 : it->second;
+    };
+    struct Op {
+        int lo, hi, r, s, i, j;  // hi < 0: scalar use of tap lo
+    };
+    std::vector<Op> ops;
+    // greedy pairing walks the taps in the step direction (a chain d, d+step, d+2 step, ...)
+    std::vector<int> order(ds);
+    auto proj = [&](int d) { return g.taps[d].dh * sh + g.taps[d].dw * sw; };
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return proj(a) != proj(b) ? proj(a) < proj(b) : a < b; });
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+            std::set<int> used;
+            for (int d : order) {
+                if (used.count(d)) continue;
+                const int i = r + g.taps[d].dh, j = s + g.taps[d].dw;
+                const int nx = next_of(d);
+                if (nx >= 0 && !used.count(nx) && is_lo(i, j)) {
+                    ops.push_back({d, nx, r, s, i, j});
+                    used.insert(d), used.insert(nx);
+                } else {
+                    ops.push_back({d, -1, r, s, i, j});
+                    used.insert(d);
+                }
+            }
+        }
+    // pixel rows in order: bounded pixel liveness
+    std::stable_sort(ops.begin(), ops.end(), [&](const Op &a, const Op &b) {
+        return std::min(a.i, a.i + (a.hi >= 0 ? sh : 0)) < std::min(b.i, b.i + (b.hi >= 0 ? sh : 0));
+    });
+    std::set<int> pair_lo, lone;
+    for (auto &o : ops) (o.hi >= 0 ? pair_lo : lone).insert(o.lo);
+    for (int d : pair_lo) os << ind << "u64 QP" << d << " = 0ull;\n";
+    for (int d : lone) os << ind << "float QL" << d << " = 0.f;\n";
+    std::set<std::pair<int, int>> loaded, packed;
+    auto px = [&](int i, int j) {
+        const std::string n = "x" + cn(i) + "_" + cn(j);
+        if (loaded.insert({i, j}).second) os << ind << "const float " << n << " = LD(tb[" << i * g.pitch + j << "]);\n";
+        return n;
+    };
+    Chunker ch{os, ind, (int)ops.size(), chunks};
+    int k = 0;
+    for (auto &o : ops) {
+        const int before = ch.cur;
+        ch.at(k++);
+        if (ch.cur != before) loaded.clear(), packed.clear();  // values do not cross chunk scopes
+        if (o.hi >= 0) {
+            const std::string a = px(o.i, o.j), b = px(o.i + sh, o.j + sw), pn = "pp" + cn(o.i) + "_" + cn(o.j);
+            if (packed.insert({o.i, o.j}).second) os << ind << "const u64 " << pn << " = f2pack(" << a << ", " << b << ");\n";
+            os << ind << "QP" << o.lo << " = ffma2(" << pn << ", f2pack(g" << o.r << "_" << o.s << ", g" << o.r << "_" << o.s
+               << "), QP" << o.lo << ");\n";
+        } else {
+            const std::string a = px(o.i, o.j);
+            os << ind << "QL" << o.lo << " = fmaf(g" << o.r << "_" << o.s << ", " << a << ", QL" << o.lo << ");\n";
+        }
+    }
+    ch.end();
+    std::map<int, int> hi_of;  // tap -> the pair in which it is the high half
+    for (auto &o : ops)
+        if (o.hi >= 0) hi_of[o.hi] = o.lo;
+    for (int d : ds) {
+        std::vector<std::string> t;
+        if (pair_lo.count(d)) t.push_back("f2lo(QP" + std::to_string(d) + ")");
+        if (hi_of.count(d)) t.push_back("f2hi(QP" + std::to_string(hi_of[d]) + ")");
+        if (lone.count(d)) t.push_back("QL" + std::to_string(d));
+        os << ind << "const float q" << d << " = ";
+        if (t.empty()) os << "0.f";
+        for (size_t q = 0; q < t.size(); ++q) os << (q ? " + " : "") << t[q];
+        os << ";\n";
+    }
+}
+
+// pair step for the packed wgrad: the displacement with the most paired products
+std::pair<int, int> pp_step(const Geo &g, const std::vector<int> &ds) {
+    const std::pair<int, int> cand[] = {{0, 1}, {1, 0}, {-1, 1}, {1, 1}};
+    std::pair<int, int> best = cand[0];
+    long bestn = -1;
+    std::set<std::pair<int, int>> o;
+    for (int d : ds) o.insert({g.taps[d].dh, g.taps[d].dw});
+    for (auto c : cand) {
+        long n = 0;  // adjacent pairs along c (the greedy pairs ~ half of the uses of each adjacent pair)
+        for (int d : ds) n += o.count({g.taps[d].dh + c.first, g.taps[d].dw + c.second});
+        if (n > bestn) bestn = n, best = c;
+    }
+    return best;
+}
+
+// pair axis of a table for the packed wgrad: the axis with more adjacent tap pairs
+int run_axis(const Geo &g) {
+    std::set<std::pair<int, int>> o;
+    for (auto &t : g.taps) o.insert({t.dh, t.dw});
+    int h = 0, v = 0;
+    for (auto &t : g.taps) h += o.count({t.dh, t.dw - 1}), v += o.count({t.dh - 1, t.dw});
+    return h >= v ? 0 : 1;
+}
+
 // backward_weight, v2: x tiles through the slot ring, dy planes through one slot
 // per pair (released right after the pair copied its dy blocks to registers).
 std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
@@ -1302,7 +1527,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     emit_header(os, x, table_of, count);
     const std::vector<Geo> geo = geo2(geo_in, L);
     const int nthreads = 32 * (L.ncw() + 1);
-    g_chunks = (env_int("O1D_WARM", 2) & 2) ? std::min(32, L.ncw()) : 0;  // bit 2: wgrad warm-up (measured: on)
+    g_chunks = (env_int("O1D_WARM", 0) & 2) ? std::min(32, L.ncw()) : 0;  // bit 2: wgrad warm-up (off: see stencil)
     const int es = x.act == O1D_F32 ? 4 : 2;
     int maxd = 0;
     for (int t = 0; t < x.nt; ++t) maxd = std::max(maxd, (int)geo[t].taps.size());
@@ -1352,6 +1577,17 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
            << "      const act_t* tb = reinterpret_cast<const act_t*>(tile) + (" << R << " * br) * " << L.pitch << " + " << S
            << " * bc;\n";
         const std::vector<int> ds = group_taps(g, 0, 1);
+        const int wgm = env_int("O1D_WG_FFMA2", 2);  // 2: pixel pairs (default), 1: dy pairs, 0: scalar
+        if (wgm) {
+            if (wgm == 2) {
+                const std::pair<int, int> st = pp_step(g, ds);
+                emit_wgrad_compute_pp(os, g, ds, st.first, st.second, "      ", g_chunks);
+            }
+            else emit_wgrad_compute_runs(os, g, ds, run_axis(g), "      ", g_chunks);
+            for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] = q" << ds[k] << ";\n";
+            os << "      break;\n    }\n";
+            continue;
+        }
         for (int d : ds) os << "      float q" << d << " = 0.f;\n";
         int npx = 0, ipx = 0;
         for_each_pixel(g, ds, [&](int, int, const std::vector<std::pair<int, std::pair<int, int>>> &) { ++npx; });
