@@ -277,6 +277,12 @@ __device__ __forceinline__ void mbar_expect_tx(u64* b, u32 bytes) {
 __device__ __forceinline__ void mbar_expect(u64* b, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sa(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ bool mbar_test(u64* b, u32 ph) {  // non-blocking: phase with parity ph completed?
+  u32 r;
+  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(r) : "r"(sa(b)), "r"(ph) : "memory");
+  return r != 0;
+}
 __device__ __forceinline__ void mbar_wait(u64* b, u32 ph) {
   // try_wait with a suspend-time hint: the warp sleeps until the phase completes
   // instead of spinning (spin loops steal issue slots from the compute warps)
@@ -350,6 +356,22 @@ __device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigne
   }
   return -1;
 }
+// v2 scheduler (producer lane 0): items are taken in batches of GB consecutive
+// indices of the current table with the next batch's atomic always in flight, so
+// a producer serving several consumer pairs is not limited to one item per
+// atomic round trip (~1 us under load)
+__device__ __forceinline__ int sched2_next(unsigned* sched, int& tcur, unsigned& lo, unsigned& hi, unsigned& nxt,
+                                           int& tried, bool steal) {
+  while (tcur >= 0) {
+    if (lo < hi && lo < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)(lo++);
+    if (nxt < (unsigned)COUNT[tcur]) { lo = nxt; hi = nxt + GB; nxt = atomicAdd(sched + tcur, (unsigned)GB); continue; }
+    if (++tried >= NT || !STEAL || !steal) { tcur = -1; break; }
+    tcur = tcur + 1 == NT ? 0 : tcur + 1;
+    lo = hi = 0;
+    nxt = atomicAdd(sched + tcur, (unsigned)GB);
+  }
+  return -1;
+}
 __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
   if (tcur >= 0) raw = atomicAdd(sched + tcur, 1u);
 }
@@ -403,6 +425,7 @@ struct Ctx {
 
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
     os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define STEAL " << (x.steal ? 1 : 0) << "\n"
+       << "#define GB " << std::max(1, env_int("O1D_GRAB", 1)) << "\n"
        << "#define CMAJOR " << env_int("O1D_CMAJOR", 1) << "\n";
     // tile reads: fp32 copy (convert path) or the raw activation tile
     os << (x.convert ? "#define LDT(v) (v)\n" : "#define LDT(v) LD(v)\n");
@@ -1067,7 +1090,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 // soon as its dy block is in registers.
 // ---------------------------------------------------------------------------
 struct Lay2 {
-    int NS = 3, P = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
+    int NS = 3, NB = 2, P = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
     size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
            total = 0;
     int ncw() const { return P * wpg; }
@@ -1101,9 +1124,10 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.sb = wgrad ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
     L.off_dy = L.off_stg + (size_t)L.ncw() * L.sb;
     L.off_t = (L.off_dy + (size_t)L.P * L.db + 1023) & ~(size_t)1023;
-    const size_t budget = (size_t)env_int("O1D_SMEM_KB", 220) * 1024;
+    const size_t budget = (size_t)env_int("O1D_SMEM_KB", 227) * 1024 - 64;
     const int fit = budget > L.off_t + L.zb ? (int)((budget - L.off_t - L.zb) / (L.zb + L.tb)) : 0;
-    L.NS = std::min(std::min(fit, NSmax), env_int("O1D_NS", 3 * L.P));
+    L.NB = std::max(1, std::min(env_int("O1D_NBUF", 2), std::min(fit, NSmax) / L.P));  // slots per pair
+    L.NS = L.P * L.NB;
     L.total = L.off_t + (size_t)L.NS * (L.zb + L.tb) + L.zb;
     return L;
 }
@@ -1135,52 +1159,86 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
        << "  __syncthreads();\n";
 }
 
-// producer warp.  Item it goes to slot it % NS (reused once the pair that had
-// item it - NS released it) and pair it % P; after the scheduler runs dry,
-// P end markers (-1) are published so every pair stops.
+// producer warp.  Each consumer pair q owns NB slots (q * NB .. q * NB + NB - 1);
+// its j-th item goes to slot q * NB + j % NB.  The producer serves the pairs
+// round-robin and never blocks on one pair: a pair whose next slot is still
+// busy (test_wait on its empty barrier) is skipped until later, so a slow pair
+// cannot hold up the loads of the others (measured with a single FIFO ring:
+// head-of-line blocking left consumers waiting ~20% of the time).  After the
+// scheduler runs dry every pair gets an end marker (-1).
 void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool wgrad, int es) {
-    const int NS = L.NS, P = L.P;
+    const int NB = L.NB, P = L.P;
     const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0);  // exact box bytes
-    os << "  if (warp == 0) {\n"
+    os << "#define P_NB " << P * NB << "\n"
+       << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
        << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
-       << "    unsigned base = 0;   // the first NS items are grabbed with one atomic (fills the ring without round trips)\n"
+       << "    unsigned lo = 0, hi = 0, nxt = 0;   // the first P*NB items come in one batch (fills the ring without round trips)\n"
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n"
-       << "      base = atomicAdd(p.sched + tcur, " << NS << "u);\n"
-       << "      raw = atomicAdd(p.sched + tcur, 1u);\n"
+       << "      lo = atomicAdd(p.sched + tcur, " << P * NB << "u); hi = lo + " << P * NB << ";\n"
+       << "      nxt = atomicAdd(p.sched + tcur, " << (env_int("O1D_SCHED2", 0) ? "(unsigned)GB" : "1u") << ");\n"
        << "    }\n"
-       << "    int ends = 0;\n"
-       << "    for (int it = 0;; ++it) {\n"
-       << "      const int s = it % " << NS << ";\n"
-       << "      if (it >= " << NS << ") mbar_wait(empty + s, ((it / " << NS << ") & 1) ^ 1);   // pair done with item it - NS\n"
-       << "      int item = -1;\n"
-       << "      if (lane == 0 && ends == 0) {\n"
-       << "        if (it < " << NS << " && base + it < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(base + it);\n"
-       << "        else { item = sched_resolve(p.sched, tcur, raw, tried, p.only < 0); sched_prefetch(p.sched, tcur, raw); }\n"
-       << "      }\n"
-       << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
-       << "      int t2 = 0, c2 = 0, n2 = 0;\n"
-       << "      if (item >= 0) item_cn(item, t2, c2, n2);\n";
-    if (wgrad)  // the pair's dy slot is free once it copied the dy block of item it - P
-        os << "      if (item >= 0 && it >= " << P << ") mbar_wait(dyempty + it % " << P << ", ((it / " << P << ") & 1) ^ 1);\n";
-    os << "      if (lane == 0) {\n"
-       << "        s_item[s] = item;\n"
-       << "        if (item >= 0) {\n"
-       << "          trace_ev(p.trace, 1, item, trn);\n"
-       << "          mbar_expect_tx(full + s, " << bytes << "u);\n"
-       << "          tma_load_ef(tiles + " << L.zb << " + s * " << L.zb + L.tb << ", &p.in_map[0], 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
+       << "    (void)raw;\n"
+       << "    int jq[" << P << "];   // items issued per pair (-1: end marker sent)\n"
+       << "    for (int q = 0; q < " << P << "; ++q) jq[q] = 0;\n"
+       << "    int issued = 0, live = " << P << ", idle = 0;\n"
+       << "    while (live > 0) {\n"
+       << "      bool any = false;\n"
+       << "#pragma unroll 1\n"
+       << "      for (int q = 0; q < " << P << "; ++q) {\n"
+       << "        const int j = jq[q];\n"
+       << "        if (j < 0) continue;\n"
+       << "        const int s = q * " << NB << " + j % " << NB << ";\n"
+       << "        if (j >= " << NB << " && !mbar_test(empty + s, ((j / " << NB << ") & 1) ^ 1)) continue;   // slot still in use\n";
+    if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
+        os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
+    os << "        int item = -1;\n"
+       << (env_int("O1D_SCHED2", 0)
+               ? "        if (lane == 0) item = sched2_next(p.sched, tcur, lo, hi, nxt, tried, p.only < 0);\n"
+               : "        if (lane == 0) {\n"
+                 "          if (issued < P_NB && lo + issued < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + issued);\n"
+                 "          else { item = sched_resolve(p.sched, tcur, nxt, tried, p.only < 0); sched_prefetch(p.sched, tcur, nxt); }\n"
+                 "        }\n")
+       << "        item = __shfl_sync(0xffffffffu, item, 0);\n"
+       << "        ++issued;\n"
+       << "        int t2 = 0, c2 = 0, n2 = 0;\n"
+       << "        if (item >= 0) item_cn(item, t2, c2, n2);\n"
+       << "        if (lane == 0) {\n"
+       << "          s_item[s] = item;\n"
+       << "          if (item >= 0) {\n"
+       << "            trace_ev(p.trace, 1, item, trn);\n"
+       << "            mbar_expect_tx(full + s, " << bytes << "u);\n"
+       << "            tma_load_ef(tiles + " << L.zb << " + s * " << L.zb + L.tb << ", &p.in_map[0], 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
     if (wgrad)
-        os << "          tma_load_ef(smem + " << L.off_dy << " + (it % " << P << ") * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
-    os << "        }\n"
-       << "      }\n";
-    if (!wgrad)
-        os << "      if (item >= 0)\n"
-           << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
-    os << "      mbar_arrive(full + s);   // 32 producer arrivals (+ the bytes) complete the phase\n"
-       << "      if (item < 0 && ++ends == " << P << ") break;\n"
+        os << "            tma_load_ef(smem + " << L.off_dy << " + q * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s" << (EFH ? ", pol);\n" : ", 0ull);\n");
+    os << "          }\n"
+       << "        }\n";
+    if (!wgrad && !env_int("O1D_WASYNC", 0)) {
+        os << "        if (item >= 0)\n"
+           << "          for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n"
+           << "        mbar_arrive(full + s);   // 32 producer arrivals (+ the bytes) complete the phase\n";
+    } else if (!wgrad) {
+        // weights: asynchronous 4-byte copies whose completion arrives on the slot's barrier
+        // (the producer never waits for them: a synchronous load here serialised the producer
+        // on one L2 round trip per item)
+        os << "        if (item >= 0) {\n"
+           << "          for (int k = lane; k < " << x.K << "; k += 32)\n"
+           << "            asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: \"r\"(sa(wsm + s * 64 + k)), \"l\"(p.w + c2 * " << x.K << " + k) : \"memory\");\n"
+           << "          asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(sa(full + s)) : \"memory\");\n"
+           << "        } else {\n"
+           << "          mbar_arrive(full + s);\n"
+           << "        }\n";
+    } else {
+        os << "        mbar_arrive(full + s);   // 32 producer arrivals (+ the bytes) complete the phase\n";
+    }
+    os << ""
+       << "        if (item < 0) { jq[q] = -1; --live; } else { jq[q] = j + 1; }\n"
+       << "        any = true;\n"
+       << "      }\n"
+       << "      if (!any) { if (++idle > 2) __nanosleep(64); } else idle = 0;\n"
        << "    }\n"
        << "    pdl_trigger();\n"
        << "    if (lane == 0) sched_exit(p.sched);\n"
@@ -1192,11 +1250,11 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "  if (!active) { bc = 0; br = 0; }\n";
 }
 
-// consumer item-loop head (v2): it < 0 is the I-cache warm-up pass over the CTA's
-// home table (one code chunk per warp, on whatever the slot holds; results dropped)
+// consumer item-loop head (v2): j is the pair's item index; j < 0 is the optional
+// I-cache warm-up pass over the CTA's home table (one code chunk per warp)
 #define V2_LOOP_HEAD \
     "    const bool warm = it < 0;\n" \
-    "    const int s = warm ? 0 : it % " << L.NS << ";\n" \
+    "    const int s = warm ? 0 : q * " << L.NB << " + it % " << L.NB << ";\n" \
     "    int item = 0, t = 0, c = 0, n = 0;\n" \
     "    unsigned wm = 0xffffffffu;\n" \
     "    if (warm) {\n" \
@@ -1204,7 +1262,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     "      wm = " << (g_chunks > 1 ? "1u << (cw % " + std::to_string(g_chunks) + ")" : std::string("0xffffffffu")) << ";\n" \
     "    } else {\n" \
     "      if (lane == 0) trace_ev(p.trace, 2, it, trn);\n" \
-    "      mbar_wait(full + s, (it / " << L.NS << ") & 1);\n" \
+    "      mbar_wait(full + s, (it / " << L.NB << ") & 1);\n" \
     "      item = s_item[s];\n" \
     "      if (lane == 0) trace_ev(p.trace, 3, item, trn);\n" \
     "      if (item < 0) break;\n" \
@@ -1228,7 +1286,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     os << "  // -------------------------------------------------------------- consumers\n"
        << "  unsigned char* const stg = smem + " << L.off_stg << " + cw * " << L.sb << ";   // this warp's output band\n"
        << "  const int row0 = " << 4 * R << " * wg;\n"
-       << "  for (int it = q - " << L.P << ";; it += " << L.P << ") {\n"
+       << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD
        << "    unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
        << "    const float* wv = wsm + s * 64;\n";
@@ -1561,7 +1619,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "  const act_t* const dys = reinterpret_cast<const act_t*>(smem + " << L.off_dy << " + q * " << L.db << ") + (" << R
        << " * br) * " << L.dyp << " + " << S << " * bc;\n"
        << "  float v[" << NV << "];\n"
-       << "  for (int it = q - " << L.P << ";; it += " << L.P << ") {\n"
+       << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD;
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s)
@@ -2043,7 +2101,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
     for (int i = 0; i < 3; ++i) {
         const Lay2 L = lay2(x, i == 1 ? sp->bwd : sp->fwd, es, hin[i], i == 2);
         const bool want = (mask >> (i == 2 ? 1 : 0)) & 1;
-        sp->v2p[i] = want && sp->BC <= 8 && (i < 2 || maxd_all <= 32) && L.NS >= L.P + 1 && L.total + 16 <= 227 * 1024;
+        sp->v2p[i] = want && sp->BC <= 8 && (i < 2 || maxd_all <= 32) && L.NB >= 2 && L.total + 16 <= 227 * 1024;
         if (sp->v2p[i]) {
             Ctx xi = x;
             xi.G = 1;

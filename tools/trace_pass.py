@@ -26,7 +26,7 @@ plan.debug_trace()
 names = ["forward", "backward_input", "backward_weight"]
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for p in range(3):
-    flush.zero_()                  # inputs come from HBM, as in bench.py (rotating buffer sets)
+    if os.environ.get("TRACE_FLUSH"): flush.zero_()  # (evicts code from L2 too: worst case)
     torch.cuda._sleep(10_000_000)  # a busy stream in front: the launch is not delayed by the host
     if p == 0: B.forward(plan, x, w)
     elif p == 1: B.backward_input(plan, dy, w)
@@ -81,7 +81,7 @@ if os.environ.get("TRACE_SM"):
 
 if os.environ.get("TRACE_TABLES"):
     for p in (0, 2):
-        flush.zero_(); torch.cuda._sleep(10_000_000)
+        torch.cuda._sleep(10_000_000)
         if p == 0: B.forward(plan, x, w)
         else: B.backward_weight(plan, x, dy, ws=ws)
         tr = plan.debug_trace()
@@ -105,7 +105,7 @@ if os.environ.get("TRACE_TABLES"):
             print(f"   table {tt}: SMs {len(np.unique(sm[mm]))}, items {mm.sum()}, ends {t[mm].min()/1e3:.1f} .. {t[mm].max()/1e3:.1f}, taps {np.median(dur.get(int(tt), [0]))/1e3:.2f}")
 
 if os.environ.get("TRACE_FIRST"):
-    flush.zero_(); torch.cuda._sleep(10_000_000)
+    torch.cuda._sleep(10_000_000)
     B.forward(plan, x, w)
     tr = plan.debug_trace()
     t = tr[:, 0].astype(np.int64); tag = tr[:, 1]
@@ -132,3 +132,21 @@ if os.environ.get("TRACE_FIRST"):
     m1 = kind == 1
     print("   producer first issue (us):", round(t[m1].min()/1e3, 2), "median first per CTA:",
           round(np.median([t[m1 & (((tag >> 32) & 0xffff) == b)].min() for b in np.unique((tag[m1] >> 32) & 0xffff)])/1e3, 2))
+
+if os.environ.get("TRACE_LAT"):
+    for p in (0, 2):
+        torch.cuda._sleep(10_000_000)
+        if p == 0: B.forward(plan, x, w)
+        else: B.backward_weight(plan, x, dy, ws=ws)
+        tr = plan.debug_trace()
+        t = tr[:, 0].astype(np.int64); tag = tr[:, 1]
+        kind = (tag >> 60).astype(int); item = (tag & 0xffffffff).astype(np.int64)
+        t = t - t[kind == 0].min()
+        iss = {int(i): tt for tt, k, i in zip(t, kind, item) if k == 1}
+        rdy = {}
+        for tt, k, i in zip(t, kind, item):
+            if k == 3 and i < 2**31: rdy.setdefault(int(i), tt)
+        lat = np.array([rdy[i] - iss[i] for i in rdy if i in iss])
+        iss_t = np.array(sorted(iss.values()))
+        print(f"== {names[p]}: load latency (issue -> consumer sees data) median {np.median(lat)/1e3:.2f} us, p10 {np.percentile(lat,10)/1e3:.2f}, p90 {np.percentile(lat,90)/1e3:.2f}; "
+              f"issues over time: first {iss_t[0]/1e3:.1f} us, 50% {iss_t[len(iss_t)//2]/1e3:.1f}, last {iss_t[-1]/1e3:.1f}")
