@@ -220,6 +220,7 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 }  // namespace
 
 constexpr int kSlots = 64;  // concurrent launches per pass that can be in flight on one plan
+constexpr int kCS = 32;     // scheduler counter stride (unsigned): one 128-byte line per counter
 constexpr size_t kTraceBytes = 8 + ((size_t)32 << 20);  // count + 2^21 (time, tag) records
 
 struct SpecSet {
@@ -352,7 +353,7 @@ __device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigne
     if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
     if (++tried >= NT || !STEAL || !steal) { tcur = -1; break; }
     tcur = tcur + 1 == NT ? 0 : tcur + 1;
-    raw = atomicAdd(sched + tcur, 1u);
+    raw = atomicAdd(sched + tcur * CS, 1u);
   }
   return -1;
 }
@@ -364,16 +365,16 @@ __device__ __forceinline__ int sched2_next(unsigned* sched, int& tcur, unsigned&
                                            int& tried, bool steal) {
   while (tcur >= 0) {
     if (lo < hi && lo < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)(lo++);
-    if (nxt < (unsigned)COUNT[tcur]) { lo = nxt; hi = nxt + GB; nxt = atomicAdd(sched + tcur, (unsigned)GB); continue; }
+    if (nxt < (unsigned)COUNT[tcur]) { lo = nxt; hi = nxt + GB; nxt = atomicAdd(sched + tcur * CS, (unsigned)GB); continue; }
     if (++tried >= NT || !STEAL || !steal) { tcur = -1; break; }
     tcur = tcur + 1 == NT ? 0 : tcur + 1;
     lo = hi = 0;
-    nxt = atomicAdd(sched + tcur, (unsigned)GB);
+    nxt = atomicAdd(sched + tcur * CS, (unsigned)GB);
   }
   return -1;
 }
 __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
-  if (tcur >= 0) raw = atomicAdd(sched + tcur, 1u);
+  if (tcur >= 0) raw = atomicAdd(sched + tcur * CS, 1u);
 }
 __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   t = item >> 22;
@@ -391,9 +392,9 @@ __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
 }
 __device__ __forceinline__ void sched_exit(unsigned* sched) {
   __threadfence();
-  if (atomicAdd(sched + NT, 1u) == gridDim.x - 1) {
-    for (int t = 0; t < NT; ++t) sched[t] = 0u;
-    sched[NT] = 0u;
+  if (atomicAdd(sched + NT * CS, 1u) == gridDim.x - 1) {
+    for (int t = 0; t < NT; ++t) sched[t * CS] = 0u;
+    sched[NT * CS] = 0u;
     __threadfence();
   }
 }
@@ -426,6 +427,7 @@ struct Ctx {
 void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &table_of, const std::vector<int> &count) {
     os << "#define NT " << x.nt << "\n#define NB " << x.N << "\n#define STEAL " << (x.steal ? 1 : 0) << "\n"
        << "#define GB " << std::max(1, env_int("O1D_GRAB", 1)) << "\n"
+       << "#define CS " << kCS << "   // scheduler counters 128 bytes apart (one L2 line each: no atomic contention between tables)\n"
        << "#define CMAJOR " << env_int("O1D_CMAJOR", 1) << "\n";
     // tile reads: fp32 copy (convert path) or the raw activation tile
     os << (x.convert ? "#define LDT(v) (v)\n" : "#define LDT(v) LD(v)\n");
@@ -885,7 +887,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
        << "    // ------------------------------------------------------------ producer\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur * CS, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      // buffer b is free once every consumer warp released item it-2: a named\n"
@@ -1169,17 +1171,20 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
 void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool wgrad, int es) {
     const int NB = L.NB, P = L.P;
     const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0);  // exact box bytes
-    os << "#define P_NB " << P * NB << "\n"
+    os << "#define P_NB " << P * NB << "\n#define PREF " << std::max(1, env_int("O1D_PREF", 2)) << "\n"
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
        << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
        << "    unsigned lo = 0, hi = 0, nxt = 0;   // the first P*NB items come in one batch (fills the ring without round trips)\n"
+       << "    unsigned pf[PREF];\n"
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n"
-       << "      lo = atomicAdd(p.sched + tcur, " << P * NB << "u); hi = lo + " << P * NB << ";\n"
-       << "      nxt = atomicAdd(p.sched + tcur, " << (env_int("O1D_SCHED2", 0) ? "(unsigned)GB" : "1u") << ");\n"
+       << "      lo = atomicAdd(p.sched + tcur * CS, " << P * NB << "u); hi = lo + " << P * NB << ";\n"
+       << (env_int("O1D_SCHED2", 0) ? "      nxt = atomicAdd(p.sched + tcur * CS, (unsigned)GB);\n"
+           : env_int("O1D_PREF", 2) > 1 ? "#pragma unroll\n      for (int k = 0; k < PREF; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+                                        : "      nxt = atomicAdd(p.sched + tcur * CS, 1u);\n")
        << "    }\n"
        << "    (void)raw;\n"
        << "    int jq[" << P << "];   // items issued per pair (-1: end marker sent)\n"
@@ -1196,7 +1201,25 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
         os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
     os << "        int item = -1;\n"
-       << (env_int("O1D_SCHED2", 0)
+       << (env_int("O1D_PREF", 2) > 1 && !env_int("O1D_SCHED2", 0)
+               ? "        if (lane == 0) {\n"
+                 "          // PREF single-item atomics in flight: each issue consumes the oldest one\n"
+                 "          if (issued < P_NB && lo + issued < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + issued);\n"
+                 "          else {\n"
+                 "            unsigned v = pf[0];\n"
+                 "#pragma unroll\n"
+                 "            for (int k = 0; k + 1 < PREF; ++k) pf[k] = pf[k + 1];\n"
+                 "            const int t0 = tcur;\n"
+                 "            item = sched_resolve(p.sched, tcur, v, tried, p.only < 0);\n"
+                 "            if (tcur != t0) {   // moved to another table: the prefetched indices belong to the old one\n"
+                 "#pragma unroll\n"
+                 "              for (int k = 0; k < PREF; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                 "            } else {\n"
+                 "              pf[PREF - 1] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+                 "            }\n"
+                 "          }\n"
+                 "        }\n"
+               : env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) item = sched2_next(p.sched, tcur, lo, hi, nxt, tried, p.only < 0);\n"
                : "        if (lane == 0) {\n"
                  "          if (issued < P_NB && lo + issued < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + issued);\n"
@@ -1840,7 +1863,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "  if (warp == 0) {\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
-       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur, 1u); }\n"
+       << "    if (lane == 0) { trace_ev(p.trace, 0, -1, trn); tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME]; raw = atomicAdd(p.sched + tcur * CS, 1u); }\n"
        << "    for (int it = 0;; ++it) {\n"
        << "      const int b = it & 1;\n"
        << "      if (it >= 2) asm volatile(\"bar.sync %0, %1;\" :: \"r\"(14 + b), \"r\"(" << 32 * (ncw + 1) << ") : \"memory\");\n"
@@ -2216,7 +2239,7 @@ o1d_status spec_create(o1d_plan *pl) {
         size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
         sp->regs[i] = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
     }
-    const size_t nsched = (size_t)3 * kSlots * (sp->nt + 1) + d.C;
+    const size_t nsched = (size_t)3 * kSlots * (sp->nt + 1) * kCS + d.C;
     if (cudaMalloc(&sp->d_sched, sizeof(unsigned) * nsched) != cudaSuccess ||
         cudaMemset(sp->d_sched, 0, sizeof(unsigned) * nsched) != cudaSuccess) {
         for (int j = 0; j < 3; ++j) dr.moduleUnload(sp->mod[j]);
@@ -2283,8 +2306,8 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[1] = const_cast<void *>(b);
     ptrs[2] = ws;
     const unsigned slot = const_cast<SpecSet *>(sp)->launch_seq.fetch_add(1) % kSlots;
-    ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + slot) * (nt + 1);
-    ptrs[4] = sp->d_sched + (size_t)3 * kSlots * (nt + 1);
+    ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + slot) * (nt + 1) * kCS;
+    ptrs[4] = sp->d_sched + (size_t)3 * kSlots * (nt + 1) * kCS;
     ptrs[5] = dW;
     int *only = reinterpret_cast<int *>(ptrs + 6);
     *only = -1;
@@ -2309,7 +2332,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
         for (int t = 0; t < nt && r == CUDA_SUCCESS; ++t) {
             *only = t;
             const unsigned sl = const_cast<SpecSet *>(sp)->launch_seq.fetch_add(1) % kSlots;
-            ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + sl) * (nt + 1);
+            ptrs[3] = sp->d_sched + ((size_t)pass * kSlots + sl) * (nt + 1) * kCS;
             r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
         }
     } else {

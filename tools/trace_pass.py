@@ -150,3 +150,25 @@ if os.environ.get("TRACE_LAT"):
         iss_t = np.array(sorted(iss.values()))
         print(f"== {names[p]}: load latency (issue -> consumer sees data) median {np.median(lat)/1e3:.2f} us, p10 {np.percentile(lat,10)/1e3:.2f}, p90 {np.percentile(lat,90)/1e3:.2f}; "
               f"issues over time: first {iss_t[0]/1e3:.1f} us, 50% {iss_t[len(iss_t)//2]/1e3:.1f}, last {iss_t[-1]/1e3:.1f}")
+
+if os.environ.get("TRACE_REACT"):
+    for p in (0, 2):
+        torch.cuda._sleep(10_000_000)
+        if p == 0: B.forward(plan, x, w)
+        else: B.backward_weight(plan, x, dy, ws=ws)
+        tr = plan.debug_trace()
+        t = tr[:, 0].astype(np.int64); tag = tr[:, 1]
+        kind = (tag >> 60).astype(int); item = (tag & 0xffffffff).astype(np.int64)
+        key = ((tag >> 32) & 0xffff).astype(np.int64) * 16 + ((tag >> 56) & 15).astype(np.int64)
+        t = t - t[kind == 0].min()
+        iss = {int(i): tt for tt, k, i in zip(t, kind, item) if k == 1}
+        gaps, waits_after = [], []
+        for k in np.unique(key[kind == 4]):
+            mk = (key == k)
+            seq3 = [(tt, int(i)) for tt, kk, i in sorted(zip(t[mk], kind[mk], item[mk])) if kk == 3 and i < 2**31]
+            seq4 = [(tt, int(i)) for tt, kk, i in sorted(zip(t[mk], kind[mk], item[mk])) if kk == 4 and i < 2**31]
+            for a in range(len(seq4) - 2):
+                rel, nxt = seq4[a][0], seq3[a + 2][1] if a + 2 < len(seq3) else None
+                if nxt is not None and nxt in iss: gaps.append(iss[nxt] - rel)
+        g = np.array(gaps)
+        print(f"== {names[p]}: slot release -> next load issue: median {np.median(g)/1e3:.2f} us, p10 {np.percentile(g,10)/1e3:.2f}, p90 {np.percentile(g,90)/1e3:.2f}")
