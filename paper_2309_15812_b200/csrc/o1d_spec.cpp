@@ -390,9 +390,9 @@ __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   n = i - (i / NB) * NB;
 #endif
 }
-__device__ __forceinline__ void sched_exit(unsigned* sched) {
+__device__ __forceinline__ void sched_exit(unsigned* sched, unsigned per_cta = 1) {
   __threadfence();
-  if (atomicAdd(sched + NT * CS, 1u) == gridDim.x - 1) {
+  if (atomicAdd(sched + NT * CS, 1u) == gridDim.x * per_cta - 1) {
     for (int t = 0; t < NT; ++t) sched[t * CS] = 0u;
     sched[NT * CS] = 0u;
     __threadfence();
@@ -1092,7 +1092,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 // soon as its dy block is in registers.
 // ---------------------------------------------------------------------------
 struct Lay2 {
-    int NS = 3, NB = 2, P = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
+    int NS = 3, NB = 2, P = 1, NPROD = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
     size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
            total = 0;
     int ncw() const { return P * wpg; }
@@ -1105,6 +1105,8 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.hin = Hin;
     L.P = std::max(1, std::min(8, env_int("O1D_P", std::max(1, 8 / x.wpg))));
     while (L.P * L.wpg > 15) --L.P;
+    L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", 2)));
+    while (L.P % L.NPROD) --L.NPROD;   // producers serve P / NPROD pairs each
     for (auto &g : geo) {
         L.pitch = std::max(L.pitch, g.pitch);
         L.zrows = std::max(L.zrows, std::max(-g.minDH, R * x.BR - Hin + g.maxDH) + 1);
@@ -1171,8 +1173,10 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
 void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool wgrad, int es) {
     const int NB = L.NB, P = L.P;
     const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0);  // exact box bytes
-    os << "#define P_NB " << P * NB << "\n#define PREF " << std::max(1, env_int("O1D_PREF", 2)) << "\n"
-       << "  if (warp == 0) {\n"
+    const int PQ = P / L.NPROD;  // pairs per producer warp (producer pw serves pairs pw, pw + NPROD, ...)
+    os << "#define P_NB " << PQ * NB << "\n#define PREF " << std::max(1, env_int("O1D_PREF", 2)) << "\n"
+       << "  if (warp < " << L.NPROD << ") {\n"
+       << "    const int pw = warp;\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
        << "    pdl_wait();\n"
        << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
@@ -1181,20 +1185,21 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n"
-       << "      lo = atomicAdd(p.sched + tcur * CS, " << P * NB << "u); hi = lo + " << P * NB << ";\n"
+       << "      lo = atomicAdd(p.sched + tcur * CS, " << PQ * NB << "u); hi = lo + " << PQ * NB << ";\n"
        << (env_int("O1D_SCHED2", 0) ? "      nxt = atomicAdd(p.sched + tcur * CS, (unsigned)GB);\n"
            : env_int("O1D_PREF", 2) > 1 ? "#pragma unroll\n      for (int k = 0; k < PREF; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
                                         : "      nxt = atomicAdd(p.sched + tcur * CS, 1u);\n")
        << "    }\n"
        << "    (void)raw;\n"
-       << "    int jq[" << P << "];   // items issued per pair (-1: end marker sent)\n"
-       << "    for (int q = 0; q < " << P << "; ++q) jq[q] = 0;\n"
-       << "    int issued = 0, live = " << P << ", idle = 0;\n"
+       << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
+       << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
+       << "    int issued = 0, live = " << PQ << ", idle = 0;\n"
        << "    while (live > 0) {\n"
        << "      bool any = false;\n"
        << "#pragma unroll 1\n"
-       << "      for (int q = 0; q < " << P << "; ++q) {\n"
-       << "        const int j = jq[q];\n"
+       << "      for (int qi = 0; qi < " << PQ << "; ++qi) {\n"
+       << "        const int q = pw + qi * " << L.NPROD << ";\n"
+       << "        const int j = jq[qi];\n"
        << "        if (j < 0) continue;\n"
        << "        const int s = q * " << NB << " + j % " << NB << ";\n"
        << "        if (j >= " << NB << " && !mbar_test(empty + s, ((j / " << NB << ") & 1) ^ 1)) continue;   // slot still in use\n";
@@ -1258,16 +1263,16 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
         os << "        mbar_arrive(full + s);   // 32 producer arrivals (+ the bytes) complete the phase\n";
     }
     os << ""
-       << "        if (item < 0) { jq[q] = -1; --live; } else { jq[q] = j + 1; }\n"
+       << "        if (item < 0) { jq[qi] = -1; --live; } else { jq[qi] = j + 1; }\n"
        << "        any = true;\n"
        << "      }\n"
        << "      if (!any) { if (++idle > 2) __nanosleep(64); } else idle = 0;\n"
        << "    }\n"
        << "    pdl_trigger();\n"
-       << "    if (lane == 0) sched_exit(p.sched);\n"
+       << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
        << "    return;\n"
        << "  }\n"
-       << "  const int cw = warp - 1, q = cw / " << L.wpg << ", wg = cw - q * " << L.wpg << ";\n"
+       << "  const int cw = warp - " << L.NPROD << ", q = cw / " << L.wpg << ", wg = cw - q * " << L.wpg << ";\n"
        << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n";
@@ -1297,7 +1302,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     std::ostringstream os;
     emit_header(os, x, table_of, count);
     const std::vector<Geo> geo = geo2(geo_in, L);
-    const int nthreads = 32 * (L.ncw() + 1);
+    const int nthreads = 32 * (L.ncw() + L.NPROD);
     // O1D_WARM bit 1: chunked I-cache warm-up for the stencils.  Off by default: with the
     // evict-first TMA traffic the code stays L2-resident and the chunk guards cost ~9% issue
     g_chunks = (env_int("O1D_WARM", 0) & 1) ? std::min(32, L.ncw()) : 0;
@@ -1607,7 +1612,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     std::ostringstream os;
     emit_header(os, x, table_of, count);
     const std::vector<Geo> geo = geo2(geo_in, L);
-    const int nthreads = 32 * (L.ncw() + 1);
+    const int nthreads = 32 * (L.ncw() + L.NPROD);
     g_chunks = (env_int("O1D_WARM", 0) & 2) ? std::min(32, L.ncw()) : 0;  // bit 2: wgrad warm-up (off: see stencil)
     const int es = x.act == O1D_F32 ? 4 : 2;
     int maxd = 0;
@@ -2202,7 +2207,7 @@ o1d_status spec_create(o1d_plan *pl) {
         xw.G = sp->gw;
         for (int i = 0; i < 3; ++i) {
             if (sp->v2p[i]) {
-                sp->smem[i] = L[i].total + 16, sp->threads[i] = 32 * (L[i].ncw() + 1);
+                sp->smem[i] = L[i].total + 16, sp->threads[i] = 32 * (L[i].ncw() + L[i].NPROD);
             } else if (i < 2) {
                 sp->smem[i] = stencil_smem(x1, i == 0 ? sp->fwd : sp->bwd);
                 sp->threads[i] = 32 * (sp->wpg * x1.G + 1);
