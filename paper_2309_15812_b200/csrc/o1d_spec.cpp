@@ -605,6 +605,31 @@ size_t stage_bytes_of(const Ctx &x) {
     return ((size_t)rows * x.Wo * 4 + 1023) & ~(size_t)1023;
 }
 
+// List schedule of independent accumulator updates: repeatedly emit the update whose
+// accumulator was used least recently (ties: original order), so dependent FMAs on one
+// accumulator are spread out (O1D_LRU=0: keep the given order).
+void emit_lru(std::ostringstream &os, const char *ind, std::vector<std::pair<std::string, std::string>> &fm,
+              std::map<std::string, long> &last_use, long &clock) {
+    if (!env_int("O1D_LRU", 1)) {
+        for (auto &f : fm) os << ind << f.second << "\n";
+        return;
+    }
+    std::vector<bool> done(fm.size(), false);
+    for (size_t n = 0; n < fm.size(); ++n) {
+        long best = -1, bt = 0;
+        for (size_t i = 0; i < fm.size(); ++i) {
+            if (done[i]) continue;
+            auto it = last_use.find(fm[i].first);
+            const long t = it == last_use.end() ? -1000000 : it->second;
+            if (best < 0 || t < bt) best = (long)i, bt = t;
+            if (t == -1000000) break;
+        }
+        done[best] = true;
+        last_use[fm[best].first] = clock++;
+        os << ind << fm[best].second << "\n";
+    }
+}
+
 // Stencil taps of group `ds` with packed FFMA2: output columns are paired
 // (s, s+1) so that the pixel pair starts at an even column relative to the
 // block: taps with even dw accumulate into pairs (0,1),(2,3),(4,5) + scalar 6
@@ -668,6 +693,8 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
     const int nrows = (int)rows.size();
     auto chunk_of = [&](int k) { return g_chunks > 1 ? (int)((long)k * g_chunks / nrows) : 0; };
     Chunker ch{os, ind, nrows, g_chunks};
+    std::map<std::string, long> last_use;
+    long clock = 0;
     for (int k = 0; k < nrows; ++k) {
         ch.at(k);
         const bool first = k == 0 || chunk_of(k - 1) != chunk_of(k);
@@ -676,27 +703,38 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
         else if (k + LA < nrows && chunk_of(k + LA) == chunk_of(k))
             loads(rows[k + LA]);
         const Row &rw = rows[k];
-        // emit slot-major (slot q of every (r, d) pair, then slot q+1, ...): consecutive
-        // instructions update different accumulators, so no FMA waits on its predecessor
+        // the row's FMAs, then a list schedule that keeps updates of one accumulator as far
+        // apart as possible (measured: near-horizontal tables put all taps of a footprint
+        // row on the same output row, and a slot-major order then chained every second
+        // FFMA2 on one accumulator: fixed-latency "wait" stalls)
+        std::vector<std::pair<std::string, std::string>> fm;  // (accumulator, statement)
         for (int q = 0; q < 4; ++q)
             for (auto &p : rw.pairs) {
                 const int r = p.first, d = p.second, dw = g.taps[d].dw;
+                std::ostringstream st;
+                std::string acc;
                 if (((dw % 2) + 2) % 2 == 0) {
                     if (q < 3) {
                         const int s = 2 * q;
-                        os << ind << "A" << r << "_" << s << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", A" << r << "_" << s << ");\n";
+                        acc = "A" + std::to_string(r) + "_" + std::to_string(s);
+                        st << acc << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", " << acc << ");";
                     } else {
-                        os << ind << "A" << r << "_6 = fmaf(" << vname(rw.i, dw + 6) << ", m" << d << ", A" << r << "_6);\n";
+                        acc = "A" + std::to_string(r) + "_6";
+                        st << acc << " = fmaf(" << vname(rw.i, dw + 6) << ", m" << d << ", " << acc << ");";
                     }
                 } else {
                     if (q < 3) {
                         const int s = 2 * q + 1;
-                        os << ind << "B" << r << "_" << s << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", B" << r << "_" << s << ");\n";
+                        acc = "B" + std::to_string(r) + "_" + std::to_string(s);
+                        st << acc << " = ffma2(" << pname(rw.i, dw + s) << ", M" << d << ", " << acc << ");";
                     } else {
-                        os << ind << "B" << r << "_0 = fmaf(" << vname(rw.i, dw) << ", m" << d << ", B" << r << "_0);\n";
+                        acc = "B" + std::to_string(r) + "_0";
+                        st << acc << " = fmaf(" << vname(rw.i, dw) << ", m" << d << ", " << acc << ");";
                     }
                 }
+                fm.push_back({acc, st.str()});
             }
+        emit_lru(os, ind, fm, last_use, clock);
     }
     ch.end();
     for (int r = 0; r < R; ++r) {
@@ -1266,7 +1304,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "        if (item < 0) { jq[qi] = -1; --live; } else { jq[qi] = j + 1; }\n"
        << "        any = true;\n"
        << "      }\n"
-       << "      if (!any) { if (++idle > 2) __nanosleep(64); } else idle = 0;\n"
+       << "      if (!any) { if (++idle > " << env_int("O1D_IDLE", 1) << ") __nanosleep(" << env_int("O1D_SLEEP", 256) << "); } else idle = 0;\n"
        << "    }\n"
        << "    pdl_trigger();\n"
        << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
