@@ -1588,21 +1588,38 @@ void emit_wgrad_compute_pp(std::ostringstream &os, const Geo &g, const std::vect
         return n;
     };
     Chunker ch{os, ind, (int)ops.size(), chunks};
+    std::map<std::string, long> last_use;
+    long clock = 0;
+    std::vector<std::pair<std::string, std::string>> fm;  // the current pixel-row group's FMAs
+    int gkey = 1 << 30;
+    auto flush = [&]() {
+        emit_lru(os, ind, fm, last_use, clock);
+        fm.clear();
+    };
     int k = 0;
+    const int nops = (int)ops.size();
     for (auto &o : ops) {
-        const int before = ch.cur;
+        const int key = std::min(o.i, o.i + (o.hi >= 0 ? sh : 0));
+        const bool new_chunk = chunks > 1 && (k == 0 || (long)k * chunks / nops != (long)(k - 1) * chunks / nops);
+        if (key != gkey || new_chunk) {  // the previous group's FMAs go out before a new group / chunk
+            flush();
+            gkey = key;
+        }
         ch.at(k++);
-        if (ch.cur != before) loaded.clear(), packed.clear();  // values do not cross chunk scopes
+        if (new_chunk) loaded.clear(), packed.clear();  // values do not cross chunk scopes
         if (o.hi >= 0) {
             const std::string a = px(o.i, o.j), b = px(o.i + sh, o.j + sw), pn = "pp" + cn(o.i) + "_" + cn(o.j);
             if (packed.insert({o.i, o.j}).second) os << ind << "const u64 " << pn << " = f2pack(" << a << ", " << b << ");\n";
-            os << ind << "QP" << o.lo << " = ffma2(" << pn << ", f2pack(g" << o.r << "_" << o.s << ", g" << o.r << "_" << o.s
-               << "), QP" << o.lo << ");\n";
+            const std::string acc = "QP" + std::to_string(o.lo);
+            fm.push_back({acc, acc + " = ffma2(" + pn + ", f2pack(g" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", g" +
+                                   std::to_string(o.r) + "_" + std::to_string(o.s) + "), " + acc + ");"});
         } else {
             const std::string a = px(o.i, o.j);
-            os << ind << "QL" << o.lo << " = fmaf(g" << o.r << "_" << o.s << ", " << a << ", QL" << o.lo << ");\n";
+            const std::string acc = "QL" + std::to_string(o.lo);
+            fm.push_back({acc, acc + " = fmaf(g" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", " + a + ", " + acc + ");"});
         }
     }
+    flush();
     ch.end();
     std::map<int, int> hi_of;  // tap -> the pair in which it is the high half
     for (auto &o : ops)
