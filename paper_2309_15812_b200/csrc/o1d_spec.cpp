@@ -1258,7 +1258,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                  "#pragma unroll\n"
                  "              for (int k = 0; k < PREF; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
                  "            } else {\n"
-                 "              pf[PREF - 1] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+                 "              pf[PREF - 1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;   // (tcur < 0: table exhausted)\n"
                  "            }\n"
                  "          }\n"
                  "        }\n"

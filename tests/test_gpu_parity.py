@@ -216,3 +216,37 @@ def test_convnext1d_harness_trains():
     assert torch.isfinite(loss)
     for layer in convnext1d.oriented_layers(m):
         assert layer.weight.grad is not None and torch.isfinite(layer.weight.grad).all()
+
+
+def test_repeated_launches_bitwise():
+    """Hundreds of back-to-back steps without host synchronisation (as bench.py runs them)
+    give bitwise the first step's results: the persistent kernels' per-launch scheduler
+    slots are reset correctly and no item is skipped or repeated."""
+    wl = inputs.S1
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, np.array(angles), device="cuda:0")
+    g = torch.Generator(device="cuda:0").manual_seed(0)
+    x = torch.rand(wl.N, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    dy = torch.rand(wl.N, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    w = torch.rand(wl.C, wl.K, device="cuda:0", generator=g)
+    ws = B.workspace(plan)
+    y0 = B.forward(plan, x, w).clone()
+    dx0 = B.backward_input(plan, dy, w).clone()
+    dW0 = B.backward_weight(plan, x, dy, ws=ws).clone()
+    n = 240  # > 64 launch slots per pass, several times over
+    ys = torch.empty((8,) + tuple(y0.shape), device="cuda:0")
+    dxs = torch.empty((8,) + tuple(dx0.shape), device="cuda:0")
+    dWs = torch.empty((n,) + tuple(dW0.shape), device="cuda:0")
+    bad = []
+    for i in range(n):
+        B.forward(plan, x, w, ys[i % 8])
+        B.backward_input(plan, dy, w, dxs[i % 8])
+        B.backward_weight(plan, x, dy, dWs[i], ws)
+        if i % 8 == 7:
+            torch.cuda.synchronize()
+            for k in range(8):
+                if not (torch.equal(ys[k], y0) and torch.equal(dxs[k], dx0)):
+                    bad.append(i - 7 + k)
+    torch.cuda.synchronize()
+    bad += [i for i in range(n) if not torch.equal(dWs[i], dW0)]
+    assert not bad, f"steps with different results: {sorted(set(bad))[:20]}"
