@@ -1243,7 +1243,8 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "        if (j >= " << NB << " && !mbar_test(empty + s, ((j / " << NB << ") & 1) ^ 1)) continue;   // slot still in use\n";
     if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
         os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
-    os << "        int item = -1;\n"
+    os << "        if (lane == 0) trace_ev(p.trace, 6, q * 65536 + j, trn);   // slot found free\n"
+       << "        int item = -1;\n"
        << (env_int("O1D_PREF", 2) > 1 && !env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) {\n"
                  "          // PREF single-item atomics in flight: each issue consumes the oldest one\n"
@@ -2113,6 +2114,26 @@ std::vector<int> home_tables(const std::vector<int> &gpc_of_smid, const std::vec
     return home;
 }
 
+// Issue-count proxy of each table's case in a generated v2 kernel: packed and scalar
+// FMAs plus shared-memory loads between "case t: {" and its "break;" (the measured
+// per-item tap-loop times of the eight S1 tables track this within ~5%).
+std::vector<long> case_costs(const std::string &src, int nt) {
+    std::vector<long> c(nt, 1);
+    for (int t = 0; t < nt; ++t) {
+        const std::string key = "    case " + std::to_string(t) + ": {";
+        const size_t a = src.rfind(key);
+        if (a == std::string::npos) continue;
+        const size_t b = src.find("break;", a);
+        const std::string body = src.substr(a, b == std::string::npos ? std::string::npos : b - a);
+        long n = 0;
+        for (const char *tok : {"ffma2(", "fmaf(", "LD(", "LDT("}) {
+            for (size_t pos = body.find(tok); pos != std::string::npos; pos = body.find(tok, pos + 1)) ++n;
+        }
+        c[t] = std::max(1L, n);
+    }
+    return c;
+}
+
 // Host-only part: eligibility, geometry and generated sources (no CUDA calls).
 // Returns false (and no sources) when the plan is not eligible.
 bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, const std::vector<int> *gpc) {
@@ -2191,8 +2212,24 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
             sp->pitch2[i] = L.pitch;
             sp->rows2[i] = hin[i];
             sp->ns2 = L.NS;
-            src[i] = i < 2 ? gen_stencil2(xi, i == 0 ? sp->fwd : sp->bwd, table_of, sp->count, hin[i], L)
-                           : gen_wgrad2(xi, sp->fwd, table_of, sp->count, hin[i], L);
+            auto gen = [&]() {
+                return i < 2 ? gen_stencil2(xi, i == 0 ? sp->fwd : sp->bwd, table_of, sp->count, hin[i], L)
+                             : gen_wgrad2(xi, sp->fwd, table_of, sp->count, hin[i], L);
+            };
+            src[i] = gen();
+            if (gpc && !gpc->empty() && env_int("O1D_COSTW", 1) == 1) {
+                // home tables of THIS pass from its own generated code: SMs per table in proportion
+                // to planes x issue count of the table's case (packed/scalar FMAs + loads); measured:
+                // the wgrad's per-table costs differ from the stencil's (pairing varies by angle)
+                const std::vector<long> cost = case_costs(src[i], sp->nt);
+                std::vector<int> work(sp->nt);
+                long mx = 1;
+                for (long c : cost) mx = std::max(mx, c);
+                for (int t = 0; t < sp->nt; ++t)
+                    work[t] = (int)std::min<long>(1L << 30, (long)sp->count[t] * (cost[t] + 100) * 1000 / (mx + 100));
+                xi.home = home_tables(*gpc, work, sp->nt);
+                src[i] = gen();
+            }
         }
     }
     sp->v2 = sp->v2p[0] || sp->v2p[1] || sp->v2p[2];

@@ -172,3 +172,31 @@ if os.environ.get("TRACE_REACT"):
                 if nxt is not None and nxt in iss: gaps.append(iss[nxt] - rel)
         g = np.array(gaps)
         print(f"== {names[p]}: slot release -> next load issue: median {np.median(g)/1e3:.2f} us, p10 {np.percentile(g,10)/1e3:.2f}, p90 {np.percentile(g,90)/1e3:.2f}")
+
+if os.environ.get("TRACE_PROD"):
+    for p in (0, 2):
+        torch.cuda._sleep(10_000_000)
+        if p == 0: B.forward(plan, x, w)
+        else: B.backward_weight(plan, x, dy, ws=ws)
+        tr = plan.debug_trace()
+        t = tr[:, 0].astype(np.int64); tag = tr[:, 1]
+        kind = (tag >> 60).astype(int); item = (tag & 0xffffffff).astype(np.int64)
+        blk = ((tag >> 32) & 0xffff).astype(np.int64); wp = ((tag >> 56) & 15).astype(np.int64)
+        t = t - t[kind == 0].min()
+        d_iss = []
+        idle_frac = []
+        for b in np.unique(blk[kind == 6])[:40]:
+            for pw_ in (0, 1):
+                m = (blk == b) & (wp == pw_)
+                ev = sorted(zip(t[m], kind[m]))
+                last6 = None
+                for tt, kk in ev:
+                    if kk == 6: last6 = tt
+                    elif kk == 1 and last6 is not None: d_iss.append(tt - last6); last6 = None
+        d = np.array(d_iss)
+        print(f"== {names[p]}: producer detect -> issue median {np.median(d)/1e3:.2f} us, p90 {np.percentile(d,90)/1e3:.2f}, max {d.max()/1e3:.2f}")
+        # consumer release (kind 4) -> producer detect (kind 6) for the same pair/slot is harder to pair; report
+        # per CTA: number of detects and spacing
+        for b in np.unique(blk[kind == 6])[:2]:
+            m = (blk == b) & (kind == 6)
+            ts = np.sort(t[m]); print("   CTA", b, "detects", len(ts), "spacing median", round(np.median(np.diff(ts))/1e3, 2), "us")
