@@ -221,6 +221,7 @@ Geo make_geo(const int16_t *oh, const int16_t *ow, int K, bool negate, int BR, i
 
 constexpr int kSlots = 64;  // concurrent launches per pass that can be in flight on one plan
 constexpr int kCS = 32;     // scheduler counter stride (unsigned): one 128-byte line per counter
+constexpr size_t kBalBytes = 2048;  // >= sizeof(Bal) in the generated prelude (1288 B)
 constexpr size_t kTraceBytes = 8 + ((size_t)32 << 20);  // count + 2^21 (time, tag) records
 
 struct SpecSet {
@@ -241,6 +242,8 @@ struct SpecSet {
     // different streams never share counters; a slot is reset by its last CTA
     unsigned *d_sched = nullptr;
     unsigned long long *d_trace = nullptr;  // diagnostics (O1D_TRACE=1): event records of the next launches
+    unsigned char *d_bal = nullptr;         // adaptive placement state, kBalBytes per pass (v2)
+    std::vector<int> home2[3];              // initial SM -> home table per pass (v2)
     std::atomic<unsigned> launch_seq{0};
     std::string regs[3];
 };
@@ -263,7 +266,19 @@ struct Params {
   float* dW;
   int only;          // >= 0: this launch processes table `only` alone (table-sequential mode)
   u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
+  void* bal;         // v2 adaptive balance state (Bal) or null
 };
+// Adaptive placement (v2): consumers add their per-item busy cycles per table; the
+// last consumer warp of a launch turns them into per-table costs (blended with the
+// previous estimate) and rewrites the SM -> home-table map the next launch of the
+// pass starts from: SMs per table in proportion to planes x measured cost, TPC pairs
+// kept together, along the GPC-ordered SM list.  Placement only: results do not
+// depend on which SM processes a plane.
+struct Bal { u64 tsum[16]; unsigned tcnt[16]; float ema[16]; unsigned done; unsigned pad; unsigned home[256]; };
+__device__ __forceinline__ void bal_flush(void* bv, int t, u64 busy, unsigned items) {
+  Bal* b = reinterpret_cast<Bal*>(bv);
+  if (b && t >= 0 && items) { atomicAdd(&b->tsum[t], busy); atomicAdd(&b->tcnt[t], items); }
+}
 __device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n));
@@ -390,6 +405,89 @@ __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   n = i - (i / NB) * NB;
 #endif
 }
+// Called by all 32 lanes of the last consumer warp of the launch: per-table costs in
+// parallel (lane t), then every lane places its share of the TPC pairs (prefix-sum
+// search over the table works) -- no serial chain of global-memory round trips.
+__device__ void bal_exit(void* bv, int lane) {
+#if NORD > 0
+  Bal* b = reinterpret_cast<Bal*>(bv);
+  float wk = 0.f;
+  if (lane < NT) {
+    const unsigned n = *((volatile unsigned*)&b->tcnt[lane]);
+    const float ema = *((volatile float*)&b->ema[lane]);
+    const float m = n ? (float)(*((volatile u64*)&b->tsum[lane])) / (float)n : ema;
+    const float e = ema > 0.f ? 0.5f * (ema + m) : m;
+    wk = (float)COUNT[lane] * (e > 0.f ? e : 1.f);
+    b->ema[lane] = e;
+    b->tsum[lane] = 0ull;
+    b->tcnt[lane] = 0u;
+  }
+  float pre[NT + 1];
+  pre[0] = 0.f;
+#pragma unroll
+  for (int q = 0; q < NT; ++q) pre[q + 1] = pre[q] + __shfl_sync(0xffffffffu, wk, q);
+  const float tot = pre[NT];
+  unsigned have = 0u;   // tables this lane assigned at least one pair to
+  int mine[(NORD / 2 + 31) / 32];
+#pragma unroll
+  for (int k = 0; k < (NORD / 2 + 31) / 32; ++k) {
+    const int i = 2 * (lane + 32 * k);
+    mine[k] = -1;
+    if (i < NORD) {
+      const float pos = (i + 1.f) * tot / NORD;
+      int t = 0;
+      while (t < NT - 1 && pos >= pre[t + 1]) ++t;
+      mine[k] = t;
+      have |= 1u << t;
+    }
+  }
+  unsigned all_t = __reduce_or_sync(0xffffffffu, have);
+  bool cover = true;
+#pragma unroll
+  for (int q = 0; q < NT; ++q) cover = cover && (((all_t >> q) & 1u) || COUNT[q] == 0);
+  if (cover) {
+#pragma unroll
+    for (int k = 0; k < (NORD / 2 + 31) / 32; ++k) {
+      const int i = 2 * (lane + 32 * k);
+      if (i < NORD) {
+        b->home[ORDER[i]] = (unsigned)mine[k];
+        if (i + 1 < NORD) b->home[ORDER[i + 1]] = (unsigned)mine[k];
+      }
+    }
+  }
+  if (lane == 0) b->done = 0u;
+  __threadfence();
+#endif
+}
+// CTA-level accounting in shared memory: [16] u64 busy cycles, [16] u32 items, u32 warps done
+__device__ __forceinline__ void bal_flush_cta(unsigned char* sb, int t, u64 busy, unsigned items) {
+  if (t < 0 || !items) return;
+  atomicAdd(reinterpret_cast<u64*>(sb) + t, busy);
+  atomicAdd(reinterpret_cast<unsigned*>(sb + 128) + t, items);
+}
+// the last consumer warp of the CTA moves the CTA's totals to the global state (one set of
+// atomics per CTA, not per warp: per-warp global atomics serialised ~1200 warps at kernel end)
+__device__ void bal_warp_exit(void* bv, unsigned char* sb, int t, u64 busy, unsigned items, unsigned ncw, int lane) {
+  // (all lanes) lane 0 adds the warp's totals to the CTA's; the CTA's last consumer warp adds
+  // the CTA's totals to the launch's (one set of global atomics per CTA); the launch's last
+  // CTA recomputes the placement
+  int last = 0;
+  if (lane == 0) {
+    bal_flush_cta(sb, t, busy, items);
+    __threadfence_block();
+    if (atomicAdd(reinterpret_cast<unsigned*>(sb + 192), 1u) == ncw - 1) {
+      __threadfence_block();
+      for (int q = 0; q < NT; ++q) {
+        const unsigned n = *((volatile unsigned*)(sb + 128) + q);
+        if (n) bal_flush(bv, q, *((volatile u64*)sb + q), n);
+      }
+      __threadfence();
+      last = atomicAdd(&reinterpret_cast<Bal*>(bv)->done, 1u) == gridDim.x - 1;
+      __threadfence();
+    }
+  }
+  if (__shfl_sync(0xffffffffu, last, 0)) bal_exit(bv, lane);
+}
 __device__ __forceinline__ void sched_exit(unsigned* sched, unsigned per_cta = 1) {
   __threadfence();
   if (atomicAdd(sched + NT * CS, 1u) == gridDim.x * per_cta - 1) {
@@ -418,6 +516,7 @@ struct Ctx {
     int gw = 2;                                          // tap groups of the wgrad kernel
     int act = 0;                                         // activation dtype (o1d_dtype)
     std::vector<int> home;                               // home table per %smid (empty: TPC-pair fallback)
+    std::vector<int> order;                              // SMs in GPC order (adaptive placement; empty: off)
     bool steal = true;                                   // CTAs move to other tables once theirs is done
     bool convert = false;                                // 16-bit tiles widened to an fp32 smem copy
     bool v2 = false;                                     // v2 pipeline (see gen_stencil2)
@@ -460,6 +559,12 @@ void emit_header(std::ostringstream &os, const Ctx &x, const std::vector<int> &t
     os << "};\n";
     // home table per SM (see home_tables()); fallback without a topology probe:
     // (smid / 2) mod NT, i.e. TPC pairs share a table
+    os << "#define NORD " << x.order.size() << "\n";
+    if (!x.order.empty()) {
+        os << "__constant__ unsigned char ORDER[" << x.order.size() << "] = {";
+        for (size_t i = 0; i < x.order.size(); ++i) os << (i ? "," : "") << x.order[i];
+        os << "};\n";
+    }
     const int nh = x.home.empty() ? x.nsm : (int)x.home.size();
     os << "#define NHOME " << nh << "\n__constant__ unsigned char HOME[" << nh << "] = {";
     for (int s = 0; s < nh; ++s) os << (s ? "," : "") << (x.home.empty() ? (s / 2) % x.nt : x.home[s]);
@@ -1131,7 +1236,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 // ---------------------------------------------------------------------------
 struct Lay2 {
     int NS = 3, NB = 2, P = 1, NPROD = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
-    size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
+    size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_bal = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
            total = 0;
     int ncw() const { return P * wpg; }
     size_t slot(int s) const { return off_t + zb + (size_t)s * (zb + tb); }
@@ -1160,7 +1265,8 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     // header: full[NSmax], empty[NSmax], dyempty[8] mbarriers | s_item | weights | scratch | dy slots | zero rows + slots
     const int NSmax = 16;
     L.off_item = 8 * (2 * (size_t)NSmax + 8);
-    L.off_w = (L.off_item + 4 * (size_t)NSmax + 15) & ~(size_t)15;
+    L.off_bal = (L.off_item + 4 * (size_t)NSmax + 15) & ~(size_t)15;  // CTA placement accounting (adaptive)
+    L.off_w = L.off_bal + 16 * 8 + 16 * 4 + 16;
     L.off_scr = L.off_w + (wgrad ? 0 : (size_t)NSmax * 64 * 4);
     L.off_stg = (L.off_scr + (wgrad ? (size_t)L.ncw() * 32 * 4 : 0) + 127) & ~(size_t)127;
     L.sb = wgrad ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
@@ -1193,6 +1299,7 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
        << "  int trn = 0;\n"
        << "  for (int i = tid; i < " << (L.total - L.off_t) / 16 << "; i += " << nthreads << ")  // zero rows + slots\n"
        << "    reinterpret_cast<uint4*>(tiles)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
+       << "  if (tid < " << (16 * 8 + 16 * 4 + 16) / 4 << ") reinterpret_cast<unsigned*>(smem + " << L.off_bal << ")[tid] = 0u;\n"
        << "  if (tid == 0) {\n"
        << "    for (int s = 0; s < " << L.NS << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << L.wpg << "); }\n";
     if (wgrad) os << "    for (int q = 0; q < " << L.P << "; ++q) mbar_init(dyempty + q, " << L.wpg << ");\n";
@@ -1222,7 +1329,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "    unsigned pf[PREF];\n"
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
-       << "      tcur = p.only >= 0 ? p.only : HOME[smid() % NHOME];\n"
+       << "      tcur = p.only >= 0 ? p.only : (p.bal ? (int)reinterpret_cast<const Bal*>(p.bal)->home[smid() % NHOME] : (int)HOME[smid() % NHOME]);\n"
        << "      lo = atomicAdd(p.sched + tcur * CS, " << PQ * NB << "u); hi = lo + " << PQ * NB << ";\n"
        << (env_int("O1D_SCHED2", 0) ? "      nxt = atomicAdd(p.sched + tcur * CS, (unsigned)GB);\n"
            : env_int("O1D_PREF", 2) > 1 ? "#pragma unroll\n      for (int k = 0; k < PREF; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
@@ -1336,6 +1443,15 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     "      item_cn(item, t, c, n);\n" \
     "    }\n"
 
+// adaptive placement accounting (per consumer warp): busy cycles per item of table t
+#define BAL_ITEM_END \
+    (x.order.empty() ? "" : \
+    "    if (t != bt) { if (lane == 0) bal_flush_cta(smem + " + std::to_string(L.off_bal) + ", bt, busy, nbusy); bt = t; busy = 0; nbusy = 0; }\n" \
+    "    busy += (u64)(clock64() - tb0); ++nbusy;\n")
+#define BAL_EXIT \
+    (x.order.empty() ? std::string() : \
+    "  if (p.bal) bal_warp_exit(p.bal, smem + " + std::to_string(L.off_bal) + ", bt, busy, nbusy, " + std::to_string(L.ncw()) + "u, lane);\n")
+
 std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
                          const std::vector<int> &count, int Hin, const Lay2 &L) {
     std::ostringstream os;
@@ -1353,8 +1469,10 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     os << "  // -------------------------------------------------------------- consumers\n"
        << "  unsigned char* const stg = smem + " << L.off_stg << " + cw * " << L.sb << ";   // this warp's output band\n"
        << "  const int row0 = " << 4 * R << " * wg;\n"
+       << (x.order.empty() ? "" : "  int bt = -1; u64 busy = 0; unsigned nbusy = 0;   // adaptive placement accounting\n")
        << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD
+       << (x.order.empty() ? "" : "    const long long tb0 = clock64();\n")
        << "    unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
        << "    const float* wv = wsm + s * 64;\n";
     for (int r = 0; r < R; ++r)
@@ -1412,8 +1530,10 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
        << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
        << "    }\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+       << BAL_ITEM_END
        << "  }\n"
        << "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
+       << BAL_EXIT
        << "}\n";
     g_chunks = 0;
     return os.str();
@@ -1703,8 +1823,10 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "  const act_t* const dys = reinterpret_cast<const act_t*>(smem + " << L.off_dy << " + q * " << L.db << ") + (" << R
        << " * br) * " << L.dyp << " + " << S << " * bc;\n"
        << "  float v[" << NV << "];\n"
+       << (x.order.empty() ? "" : "  int bt = -1; u64 busy = 0; unsigned nbusy = 0;   // adaptive placement accounting\n")
        << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
-       << V2_LOOP_HEAD;
+       << V2_LOOP_HEAD
+       << (x.order.empty() ? "" : "    const long long tb0 = clock64();\n");
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s)
             os << "    const float g" << r << "_" << s << " = active ? LD(dys[" << r * L.dyp + s << "]) : 0.f;\n";
@@ -1756,7 +1878,9 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "    for (int k = lane; k < " << x.K << "; k += 32) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+       << BAL_ITEM_END
        << "  }\n"
+       << BAL_EXIT
        << "}\n";
     const int NE = x.N * L.wpg;
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
@@ -2180,12 +2304,22 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
         for (int t = 0; t < sp->nt; ++t)
             work[t] = sp->count[t] * (env_int("O1D_COSTW", 1) ? range_cost(sp->fwd[t], 0, (int)sp->fwd[t].taps.size()) + 100 : 1);
         x.home = home_tables(*gpc, work, sp->nt);
+        if (env_int("O1D_ADAPT", 0)) {  // GPC-ordered SM list for the device-side placement update
+            std::map<int, std::vector<int>> groups;
+            for (int sm = 0; sm < (int)gpc->size(); ++sm) groups[(*gpc)[sm] >= 0 ? (*gpc)[sm] : 100000 + sm].push_back(sm);
+            for (auto &gq : groups) x.order.insert(x.order.end(), gq.second.begin(), gq.second.end());
+            if (x.order.size() > 256 || sp->nt > 16) x.order.clear();
+        }
         // every table has home SMs: no stealing needed for completion
         std::vector<int> seen(sp->nt, 0);
         for (int h : x.home) seen[h] = 1;
         bool all = true;
         for (int v : seen) all = all && v;
-        x.steal = !all || env_int("O1D_STEAL", 0) != 0;
+        // fewer planes than SMs: the grid does not cover every SM, so a table's home SMs may
+        // run no CTA -> CTAs must move on to other tables once theirs is exhausted
+        const bool partial_grid = (long)d.N * d.C < 4L * nsm;  // (v1 runs up to 3 CTAs per SM)
+        x.steal = !all || partial_grid || env_int("O1D_STEAL", 0) != 0;
+        if (partial_grid) x.order.clear();  // adaptive placement assumes one CTA on every SM
     }
     x.minb = env_int("O1D_MINB", 3);
     x.gw = env_int("O1D_GW", 2);
@@ -2230,6 +2364,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
                 xi.home = home_tables(*gpc, work, sp->nt);
                 src[i] = gen();
             }
+            sp->home2[i] = xi.home;
         }
     }
     sp->v2 = sp->v2p[0] || sp->v2p[1] || sp->v2p[2];
@@ -2345,6 +2480,17 @@ o1d_status spec_create(o1d_plan *pl) {
     }
     if (env_flag("O1D_TRACE") && cudaMalloc(&sp->d_trace, kTraceBytes) == cudaSuccess)
         cudaMemset(sp->d_trace, 0, kTraceBytes);
+    if (sp->v2 && !gpc.empty() && env_int("O1D_ADAPT", 0) && cudaMalloc(&sp->d_bal, 3 * kBalBytes) == cudaSuccess) {
+        std::vector<unsigned char> init(3 * kBalBytes, 0);
+        for (int i = 0; i < 3; ++i) {
+            unsigned *home = reinterpret_cast<unsigned *>(init.data() + i * kBalBytes + 16 * 8 + 16 * 4 + 16 * 4 + 8);
+            for (size_t k = 0; k < sp->home2[i].size() && k < 256; ++k) home[k] = (unsigned)sp->home2[i][k];
+        }
+        if (cudaMemcpy(sp->d_bal, init.data(), init.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(sp->d_bal);
+            sp->d_bal = nullptr;
+        }
+    }
     pl->spec = sp;
     char buf[768];
     snprintf(buf, sizeof buf,
@@ -2364,6 +2510,7 @@ void spec_destroy(o1d_plan *pl) {
         if (sp->mod[i]) drv().moduleUnload(sp->mod[i]);
     if (sp->d_sched) cudaFree(sp->d_sched);
     if (sp->d_trace) cudaFree(sp->d_trace);
+    if (sp->d_bal) cudaFree(sp->d_bal);
     delete sp;
     pl->spec = nullptr;
 }
@@ -2380,7 +2527,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const int nt = sp->nt;
-    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 8 * sizeof(void *)];
+    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 10 * sizeof(void *)];
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(blob);
     const std::vector<Geo> &geo = pass == 1 ? sp->bwd : sp->fwd;
     // input maps (x for forward / wgrad, dy for backward_input), one box per table
@@ -2409,6 +2556,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     int *only = reinterpret_cast<int *>(ptrs + 6);
     *only = -1;
     ptrs[7] = sp->d_trace;
+    ptrs[8] = (sp->d_bal && sp->v2p[pass] && sp->home2[pass].size() > 0) ? sp->d_bal + (size_t)pass * kBalBytes : nullptr;
     void *args[] = {blob};
     CUlaunchAttribute attr[1];
     attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -2423,6 +2571,20 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     cfg.hStream = static_cast<CUstream>(stream);
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    if (ptrs[8] && env_int("O1D_ADAPT_DEBUG", 0)) {  // diagnostics: the placement state this launch starts from
+        std::vector<unsigned char> hb(kBalBytes);
+        cudaDeviceSynchronize();
+        cudaMemcpy(hb.data(), ptrs[8], kBalBytes, cudaMemcpyDeviceToHost);
+        const float *ema = reinterpret_cast<const float *>(hb.data() + 192);
+        const unsigned *home = reinterpret_cast<const unsigned *>(hb.data() + 264);
+        std::vector<int> cnt(nt, 0);
+        for (int q = 0; q < sp->nsm && q < 256; ++q) cnt[home[q] < (unsigned)nt ? home[q] : 0]++;
+        fprintf(stderr, "[o1d adapt] pass %d SMs/table:", pass);
+        for (int t = 0; t < nt; ++t) fprintf(stderr, " %d", cnt[t]);
+        fprintf(stderr, "  ema:");
+        for (int t = 0; t < nt; ++t) fprintf(stderr, " %.0f", ema[t]);
+        fprintf(stderr, "\n");
+    }
     CUresult r = CUDA_SUCCESS;
     if (env_int("O1D_SEQ", 0) != 0 && nt > 1) {
         // table-sequential: one launch per distinct table, the whole GPU on one code path at a time
