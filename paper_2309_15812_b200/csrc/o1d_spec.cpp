@@ -265,6 +265,7 @@ struct Params {
   unsigned* cnt;     // [C] per-channel epoch counters (wgrad)
   float* dW;
   int only;          // >= 0: this launch processes table `only` alone (table-sequential mode)
+  int adapt;         // 1: this launch measures per-table costs and updates the placement (every K-th launch)
   u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
   void* bal;         // v2 adaptive balance state (Bal) or null
 };
@@ -1450,7 +1451,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     "    busy += (u64)(clock64() - tb0); ++nbusy;\n")
 #define BAL_EXIT \
     (x.order.empty() ? std::string() : \
-    "  if (p.bal) bal_warp_exit(p.bal, smem + " + std::to_string(L.off_bal) + ", bt, busy, nbusy, " + std::to_string(L.ncw()) + "u, lane);\n")
+    "  if (p.bal && p.adapt) bal_warp_exit(p.bal, smem + " + std::to_string(L.off_bal) + ", bt, busy, nbusy, " + std::to_string(L.ncw()) + "u, lane);\n")
 
 std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
                          const std::vector<int> &count, int Hin, const Lay2 &L) {
@@ -2555,6 +2556,11 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     ptrs[5] = dW;
     int *only = reinterpret_cast<int *>(ptrs + 6);
     *only = -1;
+    {
+        static std::atomic<unsigned> adapt_seq{0};
+        const int k = std::max(1, env_int("O1D_ADAPT_EVERY", 8));
+        only[1] = (adapt_seq.fetch_add(1) % (unsigned)k) == 0 ? 1 : 0;
+    }
     ptrs[7] = sp->d_trace;
     ptrs[8] = (sp->d_bal && sp->v2p[pass] && sp->home2[pass].size() > 0) ? sp->d_bal + (size_t)pass * kBalBytes : nullptr;
     void *args[] = {blob};
