@@ -250,3 +250,13 @@ def test_repeated_launches_bitwise():
     torch.cuda.synchronize()
     bad += [i for i in range(n) if not torch.equal(dWs[i], dW0)]
     assert not bad, f"steps with different results: {sorted(set(bad))[:20]}"
+
+
+@pytest.mark.parametrize("v2", ["0", "1", "2"])
+def test_pipeline_variants(v2, monkeypatch):
+    """The v1 pipeline (two tap groups, 3 CTAs/SM) stays a tested fallback: O1D_V2 selects
+    per pass (bit 1 stencils, bit 2 backward_weight) at plan creation."""
+    monkeypatch.setenv("O1D_V2", v2)
+    plan, errs = run_case(2, 16, 56, 56, 31, T.direction_angles(8, 16, "cycled"), 1, torch.float32, 0,
+                          check_det=True)
+    assert "spec" in plan.describe()
