@@ -393,7 +393,7 @@ __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsign
   if (tcur >= 0) raw = atomicAdd(sched + tcur * CS, 1u);
 }
 __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
-  t = item >> 22;
+  t = (item >> 22) & 31;   // bits 27..29: batch flags (v2 wgrad)
   const int i = item & 0x3FFFFF;
 #if CMAJOR
   // consecutive items walk the table's channels first: the planes in flight on the GPU
@@ -1236,7 +1236,7 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 // soon as its dy block is in registers.
 // ---------------------------------------------------------------------------
 struct Lay2 {
-    int NS = 3, NB = 2, P = 1, NPROD = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0;
+    int NS = 3, NB = 2, P = 1, NPROD = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0, BW = 1;
     size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_bal = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
            total = 0;
     int ncw() const { return P * wpg; }
@@ -1247,6 +1247,9 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     Lay2 L;
     L.wpg = x.wpg;
     L.hin = Hin;
+    // backward_weight: a consumer pair takes BW consecutive planes (n) of one channel and
+    // reduces its tap partials once per batch (fixed order: deterministic)
+    L.BW = wgrad ? std::max(1, std::min(x.N, env_int("O1D_WB", 1))) : 1;  // (measured: 4 -> 58 us vs 51 us, register pressure)
     L.P = std::max(1, std::min(8, env_int("O1D_P", std::max(1, 8 / x.wpg))));
     while (L.P * L.wpg > 15) --L.P;
     L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", 2)));
@@ -1339,7 +1342,11 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "    (void)raw;\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
        << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
-       << "    int issued = 0, live = " << PQ << ", idle = 0;\n"
+       << (L.BW > 1 ? "    int bq[" + std::to_string(PQ) + "], eq[" + std::to_string(PQ) + "], nq[" + std::to_string(PQ) +
+                          "];   // current batch item / next plane / planes, per served pair\n"
+                          "    for (int qi = 0; qi < " + std::to_string(PQ) + "; ++qi) { bq[qi] = -1; eq[qi] = 0; nq[qi] = 0; }\n"
+                    : "")
+       << "    int issued = 0, fetched = 0, live = " << PQ << ", idle = 0;   // planes issued / scheduler items taken (lane 0)\n"
        << "    while (live > 0) {\n"
        << "      bool any = false;\n"
        << "#pragma unroll 1\n"
@@ -1352,11 +1359,19 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
         os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
     os << "        if (lane == 0) trace_ev(p.trace, 6, q * 65536 + j, trn);   // slot found free\n"
-       << "        int item = -1;\n"
+       << "        int item = -1;\n";
+    if (L.BW > 1) {
+        // batches: the scheduler hands out (channel, n-batch) items; the pair gets the batch's
+        // planes one by one, flagged first (bit 27) / last (bit 28)
+        os << "        if (bq[qi] >= 0 && eq[qi] < nq[qi]) {\n"
+           << "          item = bq[qi];\n"
+           << "        } else {\n";
+    }
+    os << ""
        << (env_int("O1D_PREF", 2) > 1 && !env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) {\n"
                  "          // PREF single-item atomics in flight: each issue consumes the oldest one\n"
-                 "          if (issued < P_NB && lo + issued < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + issued);\n"
+                 "          if (fetched < P_NB && lo + fetched < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + fetched);\n"
                  "          else {\n"
                  "            unsigned v = pf[0];\n"
                  "#pragma unroll\n"
@@ -1370,13 +1385,30 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                  "              pf[PREF - 1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;   // (tcur < 0: table exhausted)\n"
                  "            }\n"
                  "          }\n"
+                 "          ++fetched;\n"
                  "        }\n"
                : env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) item = sched2_next(p.sched, tcur, lo, hi, nxt, tried, p.only < 0);\n"
                : "        if (lane == 0) {\n"
-                 "          if (issued < P_NB && lo + issued < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + issued);\n"
+                 "          if (fetched < P_NB && lo + fetched < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + fetched);\n"
                  "          else { item = sched_resolve(p.sched, tcur, nxt, tried, p.only < 0); sched_prefetch(p.sched, tcur, nxt); }\n"
+                 "          ++fetched;\n"
                  "        }\n")
+       << (L.BW > 1 ? "          bq[qi] = __shfl_sync(0xffffffffu, item, 0); eq[qi] = 0;\n"
+                      "          if (bq[qi] >= 0) {\n"
+                      "            const int tb = bq[qi] >> 22, b = bq[qi] & 0x3FFFFF, nch = CHOFF[tb + 1] - CHOFF[tb];\n"
+                      "            nq[qi] = min(" + std::to_string(L.BW) + ", NB - (b / nch) * " + std::to_string(L.BW) + ");\n"
+                      "          }\n"
+                      "          item = bq[qi];\n"
+                      "        }\n"
+                      "        if (item >= 0) {   // plane eq of batch item: CMAJOR plane index c_idx + nch * n\n"
+                      "          const int tb = item >> 22, b = item & 0x3FFFFF, nch = CHOFF[tb + 1] - CHOFF[tb];\n"
+                      "          const int n0 = (b / nch) * " + std::to_string(L.BW) + ";\n"
+                      "          item = (tb << 22) | ((b % nch) + nch * (n0 + eq[qi])) | (eq[qi] == 0 ? (1 << 27) : 0) |\n"
+                      "                 (eq[qi] == nq[qi] - 1 ? (1 << 28) : 0);\n"
+                      "          ++eq[qi];\n"
+                      "        }\n"
+                    : "")
        << "        item = __shfl_sync(0xffffffffu, item, 0);\n"
        << "        ++issued;\n"
        << "        int t2 = 0, c2 = 0, n2 = 0;\n"
@@ -1419,7 +1451,13 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
        << "    return;\n"
        << "  }\n"
-       << "  const int cw = warp - " << L.NPROD << ", q = cw / " << L.wpg << ", wg = cw - q * " << L.wpg << ";\n"
+       << (env_int("O1D_PAIRSMSP", 1)
+               // the warps of a pair are P warp ids apart: with P = 4 they sit on the same SM
+               // sub-partition and run the same code a few instructions apart (shared L0 I-cache)
+               ? "  const int cw = warp - " + std::to_string(L.NPROD) + ", q = cw % " + std::to_string(L.P) + ", wg = cw / " +
+                     std::to_string(L.P) + ";\n"
+               : "  const int cw = warp - " + std::to_string(L.NPROD) + ", q = cw / " + std::to_string(L.wpg) + ", wg = cw - q * " +
+                     std::to_string(L.wpg) + ";\n")
        << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n";
@@ -1787,7 +1825,10 @@ int run_axis(const Geo &g) {
 std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::vector<int> &table_of,
                        const std::vector<int> &count, int Hin, const Lay2 &L) {
     std::ostringstream os;
-    emit_header(os, x, table_of, count);
+    std::vector<int> count_b(count);  // scheduler items: (channel, batch of BW planes)
+    const int NBATCH = (x.N + L.BW - 1) / L.BW;
+    for (int t = 0; t < x.nt; ++t) count_b[t] = count[t] / x.N * NBATCH;
+    emit_header(os, x, table_of, count_b);
     const std::vector<Geo> geo = geo2(geo_in, L);
     const int nthreads = 32 * (L.ncw() + L.NPROD);
     g_chunks = (env_int("O1D_WARM", 0) & 2) ? std::min(32, L.ncw()) : 0;  // bit 2: wgrad warm-up (off: see stencil)
@@ -1834,7 +1875,8 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     os << "    __syncwarp();\n"
        << "    if (lane == 0 && !warm) mbar_arrive(dyempty + q);   // dy block in registers: the pair's dy slot is free\n"
        << "    const unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
-       << "    for (int k = 0; k < " << NV << "; ++k) v[k] = 0.f;\n"
+       << (L.BW > 1 ? "    if (item & (1 << 27)) for (int k = 0; k < " + std::to_string(NV) + "; ++k) v[k] = 0.f;   // first plane of the batch\n"
+                      : "    for (int k = 0; k < " + std::to_string(NV) + "; ++k) v[k] = 0.f;\n")
        << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
@@ -1849,7 +1891,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
                 emit_wgrad_compute_pp(os, g, ds, st.first, st.second, "      ", g_chunks);
             }
             else emit_wgrad_compute_runs(os, g, ds, run_axis(g), "      ", g_chunks);
-            for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] = q" << ds[k] << ";\n";
+            for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] " << (L.BW > 1 ? "+=" : "=") << " q" << ds[k] << ";\n";
             os << "      break;\n    }\n";
             continue;
         }
@@ -1865,17 +1907,18 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
             os << " }\n";
         });
         ch.end();
-        for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] = q" << ds[k] << ";\n";
+        for (size_t k = 0; k < ds.size(); ++k) os << "      v[" << k << "] " << (L.BW > 1 ? "+=" : "=") << " q" << ds[k] << ";\n";
         os << "      break;\n    }\n";
     }
     os << "    }\n"
        << "    if (warm) continue;\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }  // x slot released\n"
+       << (L.BW > 1 ? "    if (!(item & (1 << 28))) continue;   // reduce once per batch\n" : "")
        << "    const float part = reduce_scatter_nv(v, lane);\n"
        << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
        << "    __syncwarp();\n"
-       << "    float* wsp = p.ws + ((u64)(c * " << x.N << " + n) * " << L.wpg << " + wg) * " << x.K << ";\n"
+       << "    float* wsp = p.ws + ((u64)(c * " << NBATCH << " + n / " << L.BW << ") * " << L.wpg << " + wg) * " << x.K << ";\n"
        << "    for (int k = lane; k < " << x.K << "; k += 32) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
@@ -1883,7 +1926,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "  }\n"
        << BAL_EXIT
        << "}\n";
-    const int NE = x.N * L.wpg;
+    const int NE = NBATCH * L.wpg;
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
        << "  __shared__ double part[8][64];\n"
        << "  pdl_wait();\n"
