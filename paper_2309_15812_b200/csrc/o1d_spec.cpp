@@ -650,6 +650,7 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
 // of a table otherwise takes ~10 us of instruction fetch instead of ~1.6 us).
 int g_chunks = 0;
 #define EFH (env_int("O1D_EF", 1) != 0)  // evict-first L2 hints on the streaming TMA traffic (v2)
+#define YST (env_int("O1D_YSTORE", 0) != 0)  // stencil outputs by warp copy instead of TMA band store
 struct Chunker {
     std::ostringstream &os;
     const char *ind;
@@ -1548,7 +1549,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
        << "    if (warm) continue;\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n"
-       << "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n"
+       << (YST ? "" : "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n")
        << "    __syncwarp();\n"
        << "    if (active) {\n"
        << "      act_t* const sto = reinterpret_cast<act_t*>(stg) + (" << R << " * br - row0) * " << x.Wo << " + " << S << " * bc;\n";
@@ -1558,10 +1559,22 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
             if (ragged) os << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s << " < " << x.Wo << ") ";
             os << "sto[" << r * x.Wo + s << "] = to_act(a" << r << "_" << s << ");\n";
         }
-    os << "    }\n"
-       << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-       << "    __syncwarp();\n"
-       << "    if (lane == 0 && row0 < " << x.Ho << ") {\n"
+    os << "    }\n";
+    if (YST) {
+        // O1D_YSTORE=1: the warp copies its staged band with 16-byte loads/stores (no async-proxy
+        // fence, no wait for a previous bulk store); rows are contiguous in stg and in y
+        const int band = 4 * R;
+        os << "    __syncwarp();\n"
+           << "    {\n"
+           << "      const int nr = min(" << band << ", " << x.Ho << " - row0);\n"
+           << "      const uint4* src = reinterpret_cast<const uint4*>(stg);\n"
+           << "      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<act_t*>(p.io) + ((u64)(n * " << x.C << " + c) * " << x.Ho
+           << " + row0) * " << x.Wo << ");\n"
+           << "      for (int i = lane; i < nr * " << x.Wo * es / 16 << "; i += 32) __stcs(dst + i, src[i]);\n"
+           << "    }\n"
+           << "    __syncwarp();\n";
+    }
+    os << (YST ? "    if (false) {\n" : "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n    __syncwarp();\n    if (lane == 0 && row0 < " + std::to_string(x.Ho) + ") {\n")
        << (EFH ? "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;\"\n"
                  "                   :: \"l\"(&p.out_map), \"r\"(sa(stg)), \"r\"(0), \"r\"(row0), \"r\"(c), \"r\"(n), \"l\"(policy_evict_first()) : \"memory\");\n"
                : "      asm volatile(\"cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\"\n"
