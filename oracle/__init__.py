@@ -26,7 +26,7 @@ import threading
 
 import numpy as np
 
-from .taps import direction_angles, taps_exact, taps_table  # noqa: F401
+from .taps import direction_angles, taps_exact, taps_exact_shear, taps_table  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")

@@ -69,14 +69,74 @@ def taps_exact(K: int, pad: int, theta_deg: float):
     return out
 
 
-def taps_table(K: int, pad: int, angles_deg):
-    """Per-channel tables: (oh[C][K], ow[C][K]) as nested lists of int."""
+# Shear parameterisation (Appendix "Rotation vs Shearing").  The filter
+# offset of tap k is sampled where the filter axis crosses integer columns,
+# (delta_h, delta_w) = (-(k-pad) tan t, k-pad) (shear matrix S^x), or integer
+# rows, ((k-pad), -(k-pad) cot t) (S^y); then floored as in Eq. coordinate1d.
+# Readings (R13): the column form is used when |cos t| >= |sin t| (the axis
+# is closer to horizontal), the row form otherwise; the offsets keep the direction of
+# the rotation form (-sin t, cos t) -- i.e. offset = m * (-sin t, cos t) / max(|sin t|,
+# |cos t|), m = k - pad -- so both forms agree with the rotation taps at 0 and 90 deg
+# and tap k keeps its side of the centre.  P:432's worked example (t = -45 deg,
+# pad = 0: offsets k(1, 1)) follows.
+#
+# Exactness: tan t for rational t (degrees) is rational only at t = 0, 45, 135 (mod
+# 180) (Niven), where it is 0 or +-1; there the offset is evaluated exactly.  Otherwise
+# m tan t (m != 0) is irrational and its floor is taken at 80 digits with the
+# distance to the nearest integer asserted, as for the rotation form.
+_TAN_RATIONAL = {0: Fraction(0), 45: Fraction(1), 135: Fraction(-1)}  # degrees mod 180
+
+
+def _exact_floor_shear(m: int, t: Fraction, use_cols: bool, coord: str) -> int:
+    """floor of one coordinate of m * (-sin t, cos t) / max(|sin t|, |cos t|)."""
+    if m == 0:
+        return 0
+    u = t % 180
+    sgn_cos = 1 if (t < 90 or t > 270) else (-1 if 90 < t < 270 else 0)
+    sgn_sin = 1 if 0 < t < 180 else (-1 if t > 180 else 0)
+    if use_cols:  # |cos| >= |sin|: delta_w = m sgn(cos t), delta_h = -m tan(t) sgn(cos t)
+        if coord == "w":
+            return m * sgn_cos
+        if u.denominator == 1 and int(u) in _TAN_RATIONAL:
+            v = -m * _TAN_RATIONAL[int(u)] * sgn_cos
+            return v.numerator // v.denominator
+        fn = lambda r: -m * mpmath.tan(r) * sgn_cos
+    else:  # |sin| > |cos|: delta_h = -m sgn(sin t), delta_w = m cot(t) sgn(sin t)
+        if coord == "h":
+            return -m * sgn_sin
+        if u == 90:
+            return 0
+        fn = lambda r: m * mpmath.cot(r) * sgn_sin
+    with mpmath.workdps(_DPS):
+        rad = mpmath.mpf(t.numerator) / t.denominator * mpmath.pi / 180
+        v = fn(rad)
+        f = int(mpmath.floor(v))
+        dist = min(v - f, f + 1 - v)
+        assert dist > mpmath.mpf(10) ** (-(_DPS - 20)), (m, t, coord)
+    return f
+
+
+def taps_exact_shear(K: int, pad: int, theta_deg: float):
+    """Exact shear-form tap table for one angle: list of (oh_k, ow_k)."""
+    t = _reduce_deg(theta_deg)
+    u = t % 180
+    use_cols = u <= 45 or u >= 135  # |cos t| >= |sin t|
+    return [(_exact_floor_shear(k - pad, t, use_cols, "h"), _exact_floor_shear(k - pad, t, use_cols, "w"))
+            for k in range(K)]
+
+
+def taps_table(K: int, pad: int, angles_deg, mode: str = "rotation"):
+    """Per-channel tables: (oh[C][K], ow[C][K]) as nested lists of int.  mode:
+    "rotation" (Def. 1, the paper's default) or "shear" (Appendix)."""
+    if mode not in ("rotation", "shear"):
+        raise ValueError("mode must be 'rotation' or 'shear'")
+    one = taps_exact if mode == "rotation" else taps_exact_shear
     cache = {}
     oh, ow = [], []
     for a in angles_deg:
         key = float(a)
         if key not in cache:
-            cache[key] = taps_exact(K, pad, key)
+            cache[key] = one(K, pad, key)
         t = cache[key]
         oh.append([p[0] for p in t])
         ow.append([p[1] for p in t])
