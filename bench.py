@@ -44,6 +44,8 @@ def parse():
                     help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
     ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
     ap.add_argument("--K", type=int, default=None, help="kernel length (experiments; default: the workload's 31)")
+    ap.add_argument("--disc", default="rotation", choices=["rotation", "shear"],
+                    help="tap discretisation: rotation (Def. 1) or shear (Appendix, P:386-440)")
     ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
                     help="time the ConvNeXt-1D training step (images/s) instead of the layer step")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch for --model (default 128 T / 64 B)")
@@ -287,7 +289,8 @@ def run_ours(args):
     angles = B.direction_angles(wl.D, wl.C, wl.assign)
     if args.angle is not None:
         angles = np.full(wl.C, float(args.angle))
-    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, angles, dtype=tdt, flags=args.flags, device=dev)
+    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, angles, dtype=tdt, flags=args.flags, device=dev,
+                  discretization=args.disc)
     # two rotating buffer sets so every pass streams from HBM (each set 4 x 77 MB > L2)
     sets = []
     for s in range(2):
@@ -395,7 +398,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64 U[-1,1))",
         "config": {"workload": wl.name, "N_per_gpu": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
-                   "angles": f"D={wl.D} {wl.assign}" if args.angle is None else f"all {args.angle} deg",
+                   "angles": (f"D={wl.D} {wl.assign}" if args.angle is None else f"all {args.angle} deg")
+                   + ("" if args.disc == "rotation" else f", {args.disc} taps"),
                    "stride": 1, "layout": "NCHW",
                    "parallelism": f"dp{world} (batch-sharded, NCCL all-reduce of dW)",
                    "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"},

@@ -84,6 +84,10 @@ typedef struct {
  * kernel family that supports the problem. */
 #define O1D_FLAG_FORCE_GENERIC 0x1  /* runtime-tap shared-memory kernels only (no JIT)  */
 #define O1D_FLAG_NO_TMA        0x2  /* stage tiles with plain loads instead of TMA      */
+/* Discretisation of the filter offsets (a property of the method, not a tuning option):
+ * default = rotation (Def. 1); O1D_FLAG_SHEAR = the shear parameterisation of the
+ * Appendix "Rotation vs Shearing", see o1d_make_taps_ex. */
+#define O1D_FLAG_SHEAR         0x4
 
 typedef struct o1d_plan o1d_plan;
 
@@ -97,6 +101,19 @@ typedef struct o1d_plan o1d_plan;
  * pad: -1 => floor(K/2).  Pure host function, no CUDA context needed. */
 O1D_API o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles_deg,
                          int16_t *oh, int16_t *ow);
+
+/* Tap-offset table for discretisation `mode`: O1D_TAPS_ROTATION (= o1d_make_taps) or
+ * O1D_TAPS_SHEAR (Appendix "Rotation vs Shearing"): the offsets are sampled
+ * where the filter axis crosses integer columns, (-(k-pad) tan t, k-pad) (S^x),
+ * or integer rows, ((k-pad), -(k-pad) cot t) (S^y), keeping the direction of
+ * the rotation form: offset = m (-sin t, cos t) / max(|sin t|, |cos t|), m = k - pad,
+ * the column form when |cos t| >= |sin t| (reading R13); the non-integer
+ * coordinate is floored exactly (tan t is rational only at t = 0, 45, 135 mod 180).
+ * Same arguments, ownership and errors as o1d_make_taps; INVALID_ARG for a bad mode. */
+#define O1D_TAPS_ROTATION 0
+#define O1D_TAPS_SHEAR    1
+O1D_API o1d_status o1d_make_taps_ex(int32_t K, int32_t pad, int32_t C, const double *angles_deg, int32_t mode,
+                                    int16_t *oh, int16_t *ow);
 
 /* Per-channel angles from D directions: angle_i = i*180/D deg,
  * channels split into D equal groups; group(c) = floor(c*D/C) for

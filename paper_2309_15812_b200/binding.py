@@ -24,13 +24,15 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "INVALID_SHAPE", 3: "INVALID_CONFIG", 4:
 DTYPES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 FLAG_FORCE_GENERIC = 0x1
 FLAG_NO_TMA = 0x2
+FLAG_SHEAR = 0x4
+TAPS = {"rotation": 0, "shear": 1}
 ASSIGN = {"contiguous": 0, "cycled": 1}
 
 EXPORTS = ["o1d_make_taps", "o1d_direction_angles", "o1d_plan_create", "o1d_plan_out_shape",
            "o1d_plan_get_taps", "o1d_plan_describe", "o1d_workspace_bytes", "o1d_forward",
            "o1d_backward_input", "o1d_backward_weight", "o1d_step_host_workspace_bytes", "o1d_step_host",
            "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source",
-           "o1d_debug_trace"]
+           "o1d_debug_trace", "o1d_make_taps_ex"]
 
 
 class O1DError(RuntimeError):
@@ -75,6 +77,7 @@ def lib():
                 "o1d_last_error": (ctypes.c_char_p, []),
                 "o1d_version": (ctypes.c_char_p, []),
                 "o1d_debug_trace": (ctypes.c_size_t, [vp, vp, ctypes.c_size_t]),
+                "o1d_make_taps_ex": (st, [i32, i32, i32, f64p, i32, i16p, i16p]),
                 "o1d_spec_source": (st, [ctypes.POINTER(_Desc), f64p, i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
             }
             for name, (res, args) in sig.items():
@@ -98,13 +101,16 @@ def version() -> str:
     return lib().o1d_version().decode()
 
 
-def make_taps(K: int, angles_deg, pad: int = -1):
-    """Tap tables (oh, ow) int16 [C][K] from the library's host tap generator."""
+def make_taps(K: int, angles_deg, pad: int = -1, discretization: str = "rotation"):
+    """Tap tables (oh, ow) int16 [C][K] from the library's host tap generator;
+    discretization "rotation" (Def. 1) or "shear" (Appendix, P:386-440)."""
     a = np.ascontiguousarray(angles_deg, dtype=np.float64)
     C = a.shape[0]
     oh = np.empty((C, K), np.int16)
     ow = np.empty((C, K), np.int16)
-    _check(lib().o1d_make_taps(K, pad, C, _ptr(a), _ptr(oh), _ptr(ow)))
+    if discretization not in TAPS:
+        raise ValueError("discretization must be 'rotation' or 'shear'")
+    _check(lib().o1d_make_taps_ex(K, pad, C, _ptr(a), TAPS[discretization], _ptr(oh), _ptr(ow)))
     return oh, ow
 
 
@@ -133,7 +139,12 @@ def _stream_handle(stream):
 class Plan:
     """An immutable o1d_plan for one problem shape, dtype and angle set."""
 
-    def __init__(self, N, C, H, W, K, angles_deg, stride=1, pad=-1, dtype=torch.float32, flags=0, device=None):
+    def __init__(self, N, C, H, W, K, angles_deg, stride=1, pad=-1, dtype=torch.float32, flags=0, device=None,
+                 discretization="rotation"):
+        if discretization not in TAPS:
+            raise ValueError("discretization must be 'rotation' or 'shear'")
+        if discretization == "shear":
+            flags |= FLAG_SHEAR
         a = np.ascontiguousarray(angles_deg, dtype=np.float64)
         if a.shape != (C,):
             raise ValueError("angles must have shape [C]")

@@ -64,6 +64,49 @@ static int floor_trig_times(int m, double t, bool is_sin) {
 }
 
 
+// Shear form (reading R13): offset = m (-sin t, cos t) / max(|sin t|, |cos t|).
+// The grid coordinate is exact (+-m); the other one is floor(-+m tan t) / floor(+-m cot t).
+// tan t of a rational angle is rational only at t = 0, 45, 135 (mod 180) (Niven): exact
+// there; elsewhere irrational, floored from f64 unless within 1e-9 of an integer, then in
+// binary128.
+static int floor_m_tan(int m, double t, bool cot) {  // floor(m * tan(t)) or floor(m * cot(t)), t in [0, 360)
+    if (m == 0) return 0;
+    const double u = std::fmod(t, 180.0);
+    if (!cot && (u == 0.0)) return 0;
+    if (!cot && (u == 45.0)) return m;
+    if (!cot && (u == 135.0)) return -m;
+    if (cot && u == 90.0) return 0;
+    if (cot && u == 45.0) return m;
+    if (cot && u == 135.0) return -m;
+    const double rad = t * (M_PI / 180.0);
+    const double v = (double)m * (cot ? std::cos(rad) / std::sin(rad) : std::tan(rad));
+    const double n = std::nearbyint(v);
+    if (std::fabs(v - n) >= 1e-9) return (int)std::floor(v);
+    const __float128 radq = (__float128)t * (acosq((__float128)-1) / 180);
+    const __float128 vq = (__float128)m * (cot ? cosq(radq) / sinq(radq) : tanq(radq));
+    return (int)floorq(vq);
+}
+
+void make_taps_one_shear(int K, int pad, double theta_deg, int16_t *oh, int16_t *ow) {
+    double t = std::fmod(theta_deg, 360.0);  // exact
+    if (t < 0) t += 360.0;
+    if (t >= 360.0) t -= 360.0;
+    const double u = std::fmod(t, 180.0);
+    const bool cols = u <= 45.0 || u >= 135.0;  // |cos t| >= |sin t|
+    const int sgn_cos = (t < 90.0 || t > 270.0) ? 1 : ((t > 90.0 && t < 270.0) ? -1 : 0);
+    const int sgn_sin = (t > 0.0 && t < 180.0) ? 1 : (t > 180.0 ? -1 : 0);
+    for (int k = 0; k < K; ++k) {
+        const int m = k - pad;
+        if (cols) {  // delta_w = m sgn(cos t), delta_h = -m tan(t) sgn(cos t)
+            ow[k] = (int16_t)(m * sgn_cos);
+            oh[k] = (int16_t)floor_m_tan(-m * sgn_cos, t, false);
+        } else {     // delta_h = -m sgn(sin t), delta_w = m cot(t) sgn(sin t)
+            oh[k] = (int16_t)(-m * sgn_sin);
+            ow[k] = (int16_t)floor_m_tan(m * sgn_sin, t, true);
+        }
+    }
+}
+
 void make_taps_one(int K, int pad, double theta_deg, int16_t *oh, int16_t *ow) {
     double t = std::fmod(theta_deg, 360.0);  // exact
     if (t < 0) t += 360.0;
@@ -93,6 +136,22 @@ o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles
     for (int c = 0; c < C; ++c) {
         if (!std::isfinite(angles_deg[c])) return fail(O1D_INVALID_ARG, "o1d_make_taps: non-finite angle");
         make_taps_one(K, pad, angles_deg[c], oh + (size_t)c * K, ow + (size_t)c * K);
+    }
+    return O1D_OK;
+}
+
+o1d_status o1d_make_taps_ex(int32_t K, int32_t pad, int32_t C, const double *angles_deg, int32_t mode, int16_t *oh,
+                            int16_t *ow) {
+    if (mode == O1D_TAPS_ROTATION) return o1d_make_taps(K, pad, C, angles_deg, oh, ow);
+    if (mode != O1D_TAPS_SHEAR) return fail(O1D_INVALID_ARG, "o1d_make_taps_ex: mode must be O1D_TAPS_ROTATION or O1D_TAPS_SHEAR");
+    if (!angles_deg || !oh || !ow) return fail(O1D_INVALID_ARG, "o1d_make_taps_ex: NULL pointer");
+    if (K < 1) return fail(O1D_INVALID_CONFIG, "o1d_make_taps_ex: K < 1");
+    if (C < 1) return fail(O1D_INVALID_SHAPE, "o1d_make_taps_ex: C < 1");
+    if (pad < 0) pad = K / 2;
+    if (pad >= K) return fail(O1D_INVALID_CONFIG, "o1d_make_taps_ex: pad >= K");
+    for (int c = 0; c < C; ++c) {
+        if (!std::isfinite(angles_deg[c])) return fail(O1D_INVALID_ARG, "o1d_make_taps_ex: non-finite angle");
+        make_taps_one_shear(K, pad, angles_deg[c], oh + (size_t)c * K, ow + (size_t)c * K);
     }
     return O1D_OK;
 }
@@ -128,6 +187,8 @@ static o1d_status validate_desc(const o1d_desc *d) {
     if (d->layout != O1D_NCHW) return fail(O1D_UNSUPPORTED, "only the NCHW-contiguous layout is implemented");
     if ((long)d->N * d->C * d->H * d->W > (1L << 40)) return fail(O1D_UNSUPPORTED, "tensor too large");
     if (d->K > 1023) return fail(O1D_UNSUPPORTED, "K > 1023");
+    if (d->flags & ~(O1D_FLAG_FORCE_GENERIC | O1D_FLAG_NO_TMA | O1D_FLAG_SHEAR))
+        return fail(O1D_INVALID_ARG, "unknown bits in o1d_desc.flags");
     return O1D_OK;
 }
 
@@ -144,7 +205,9 @@ static o1d_status plan_host_init(const o1d_desc *d, const double *angles_deg, o1
     pl->angles.assign(angles_deg, angles_deg + C);
     pl->oh.resize((size_t)C * K);
     pl->ow.resize((size_t)C * K);
-    if (o1d_status st = o1d_make_taps(K, pl->pad, C, angles_deg, pl->oh.data(), pl->ow.data())) return st;
+    if (o1d_status st = o1d_make_taps_ex(K, pl->pad, C, angles_deg, (d->flags & O1D_FLAG_SHEAR) ? O1D_TAPS_SHEAR : O1D_TAPS_ROTATION,
+                                         pl->oh.data(), pl->ow.data()))
+        return st;
     std::map<std::vector<int16_t>, int> ids;
     pl->table_of.resize(C);
     pl->minOH = pl->minOW = 1 << 20;

@@ -124,3 +124,24 @@ def test_spec_source_ineligible_shapes():
     assert e.value.status == 5
     with pytest.raises(B.O1DError):
         B.spec_source(1, 8, 56, 56, 7, np.zeros(8), 0, stride=2)
+
+
+def test_make_taps_shear_bit_exact():
+    """The library's shear-form tables (o1d_make_taps_ex) equal the oracle's exact
+    tables bit for bit, incl. angles within 1e-7 deg of the 45-degree family (tan = +-1)."""
+    import random
+    from oracle import taps as T
+    rnd = random.Random(3)
+    angs = [0, 45, 90, 135, 180, -45, 22.5, 67.5, 112.5, 157.5, 30, 60, 89.999, 90.001, 44.9999999,
+            45.0000001, 134.9999999, 1e-9, -1e-9, 359.99999] + [rnd.uniform(-720, 720) for _ in range(200)]
+    angs += [i * 180 / 96 for i in range(96)] + list(range(0, 360, 7))
+    for K in (1, 3, 7, 31, 63):
+        oh, ow = B.make_taps(K, np.array(angs, float), discretization="shear")
+        roh, row = T.taps_table(K, K // 2, angs, "shear")
+        assert np.array_equal(oh, np.array(roh)) and np.array_equal(ow, np.array(row)), K
+    with pytest.raises(ValueError):
+        B.make_taps(7, np.zeros(2), discretization="bilinear")
+    import ctypes
+    a = np.zeros(2)
+    o1, o2 = np.empty((2, 7), np.int16), np.empty((2, 7), np.int16)
+    assert B.lib().o1d_make_taps_ex(7, 3, 2, a.ctypes.data, 5, o1.ctypes.data, o2.ctypes.data) == 1  # INVALID_ARG

@@ -26,17 +26,19 @@ def nerr(g: torch.Tensor, r: np.ndarray) -> float:
 _oracle_cache = {}
 
 
-def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, threads=None, check_det=False):
+def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, threads=None, check_det=False,
+             disc="rotation"):
     angles = [float(a) for a in angles]
-    plan = B.Plan(N, C, H, W, K, np.array(angles), stride=stride, dtype=dtype, flags=flags, device="cuda:0")
+    plan = B.Plan(N, C, H, W, K, np.array(angles), stride=stride, dtype=dtype, flags=flags, device="cuda:0",
+                  discretization=disc)
     P, Q = plan.P, plan.Q
     dt = NP_DT[dtype]
     x = inputs.activation((N, C, H, W), 0, dt)
     w = inputs.weights(C, K, 1)
     dy = inputs.activation((N, C, P, Q), 2, dt)
-    key = (N, C, H, W, K, tuple(angles), stride, dt)
+    key = (N, C, H, W, K, tuple(angles), stride, dt, disc)
     if key not in _oracle_cache:
-        oh, ow = T.taps_table(K, K // 2, angles)
+        oh, ow = T.taps_table(K, K // 2, angles, disc)
         oh, ow = np.array(oh, np.int32), np.array(ow, np.int32)
         th = threads or max(1, oracle.max_threads())
         _oracle_cache.clear()
@@ -260,3 +262,26 @@ def test_pipeline_variants(v2, monkeypatch):
     plan, errs = run_case(2, 16, 56, 56, 31, T.direction_angles(8, 16, "cycled"), 1, torch.float32, 0,
                           check_det=True)
     assert "spec" in plan.describe()
+
+
+
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("HW", [(56, 56), (37, 48), (14, 14)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_shear_discretization(flags, HW, stride):
+    """Shear-form tap tables (Appendix "Rotation vs Shearing"; plan flag
+    O1D_FLAG_SHEAR) through every pass vs the oracle with the same tables."""
+    H, W = HW
+    angles = T.direction_angles(8, 16, "cycled") if stride == 1 else [-45.0, 10.0, 30.0, 60.0, 100.0, 135.0, 170.0, 225.0]
+    C = len(angles) if stride != 1 else 16
+    plan, errs = run_case(2, C, H, W, 31 if stride == 1 else 7, angles, stride, torch.float32, FLAGS[flags],
+                          check_det=True, disc="shear")
+    oh, ow = plan.taps()
+    assert all(len(set(zip(oh[c], ow[c]))) == plan.K for c in range(plan.C))  # no redundant taps (P:434)
+
+
+def test_shear_full_stage1():
+    """BASELINE configs[1] shape with shear tables, in the bench launch configuration."""
+    wl = inputs.S1
+    run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, torch.float32, 0,
+             disc="shear")
