@@ -35,13 +35,15 @@ class Oriented1dDWConv(torch.nn.Module):
     """Depthwise convolution of oriented 1D kernels (Def. 1).
 
     C channels, kernel length K, D directions assigned "contiguous"
-    (paper) or "cycled"; `shift_deg` = layer-wise rotation.  Weights are
-    fp32 [C][K]; activations NCHW-contiguous fp32/bf16/fp16."""
+    (paper) or "cycled"; `shift_deg` = layer-wise rotation (P:1457);
+    `discretization` = "rotation" (Def. 1) or "shear" (Appendix, P:386-440).  Weights
+    are fp32 [C][K]; activations NCHW-contiguous fp32/bf16/fp16."""
 
     def __init__(self, C: int, K: int, D: int = 8, stride: int = 1, assign: str = "contiguous",
-                 shift_deg: float = 0.0, angles_deg=None):
+                 shift_deg: float = 0.0, angles_deg=None, discretization: str = "rotation"):
         super().__init__()
         self.C, self.K, self.stride = C, K, stride
+        self.discretization = discretization
         if angles_deg is None:
             angles_deg = B.direction_angles(D, C, assign, shift_deg)
         # kept as float64 numpy (not a buffer: Module.to(dtype) must not round the angles)
@@ -56,7 +58,7 @@ class Oriented1dDWConv(torch.nn.Module):
         p = self._plans.get(key)
         if p is None:
             p = B.Plan(N, C, H, W, self.K, self.angles_deg, stride=self.stride, dtype=x.dtype,
-                       device=x.device)
+                       device=x.device, discretization=self.discretization)
             self._plans[key] = p
         return p
 
