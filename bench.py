@@ -44,6 +44,9 @@ def parse():
                     help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
     ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
     ap.add_argument("--K", type=int, default=None, help="kernel length (experiments; default: the workload's 31)")
+    ap.add_argument("--workload", default="s1", choices=["s1", "pp_main", "pp_res"],
+                    help="s1 = BASELINE configs[1] (default); pp_main / pp_res = the 1D++ block's K=15 main and "
+                         "C=384 residual oriented convs (SURVEY NEXT-3)")
     ap.add_argument("--disc", default="rotation", choices=["rotation", "shear"],
                     help="tap discretisation: rotation (Def. 1) or shear (Appendix, P:386-440)")
     ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
@@ -181,7 +184,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2309_15812_b200 import inputs
-    wl = inputs.S1
+    wl = inputs.WORKLOADS[args.workload]
     cb = cpu_baseline(wl, args.dtype, target_s=max(2.0, 60.0 / max(1, args.steps + args.warmup)))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
@@ -279,7 +282,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.dtype]
     es = 4 if args.dtype == "f32" else 2
-    wl = inputs.S1
+    wl = inputs.WORKLOADS[args.workload]
     if args.dirs is not None:
         from dataclasses import replace
         wl = replace(wl, D=args.dirs)

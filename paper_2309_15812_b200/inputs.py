@@ -97,3 +97,12 @@ S1 = Workload("convnext_t_1d_stage1", 64, 96, 56, 56, 31, 8, "cycled")
 def ksweep(K: int) -> Workload:
     """configs[2]: kernel-length sweep at C=384, 14x14, N=128."""
     return Workload(f"ksweep_k{K}", 128, 384, 14, 14, K, 8, "cycled")
+
+
+# SURVEY NEXT-3: the 1D++ block of ConvNeXt1D++ (P:1469-1483): the block's main oriented
+# conv shrinks to K=15, and a residual depthwise oriented 1x31 conv is inserted on the
+# 4C-expanded inverted bottleneck (C = 4 x 96 = 384 at stage 1 of the T model).
+PP_MAIN = Workload("convnext_t_1dpp_stage1_main", 64, 96, 56, 56, 15, 8, "cycled")
+PP_RES = Workload("convnext_t_1dpp_stage1_residual", 64, 384, 56, 56, 31, 8, "cycled")
+
+WORKLOADS = {"s1": S1, "pp_main": PP_MAIN, "pp_res": PP_RES}

@@ -285,3 +285,13 @@ def test_shear_full_stage1():
     wl = inputs.S1
     run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, torch.float32, 0,
              disc="shear")
+
+
+@pytest.mark.parametrize("which", ["pp_main", "pp_res"])
+def test_1dpp_block_workloads(which):
+    """the 1D++ block's K=15 main conv (C=96) and its residual 1x31 conv on
+    the 4C inverted bottleneck (C=384), 56x56, D=8, at N=4 (every table
+    and the bench launch configuration; the full batch only adds planes)."""
+    wl = inputs.WORKLOADS[which]
+    run_case(4, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, torch.float32, 0,
+             check_det=True)
