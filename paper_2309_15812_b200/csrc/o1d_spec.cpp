@@ -1328,7 +1328,11 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "  if (warp < " << L.NPROD << ") {\n"
        << "    const int pw = warp;\n"
        << "    int tcur = 0, tried = 0; unsigned raw = 0;\n"
-       << "    pdl_wait();\n"
+       << "    // the scheduler counters of this launch slot were last touched 64 launches ago: the\n"
+       << "    // first atomics run before griddepcontrol.wait, overlapping the preceding kernel's tail\n"
+       << "    // (only the data -- x / dy / w -- may be produced by it)\n"
+       << "    const bool early = " << (env_int("O1D_EARLY", 1) ? "p.bal == nullptr" : "false") << ";\n"
+       << "    if (!early) pdl_wait();\n"
        << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
        << "    unsigned lo = 0, hi = 0, nxt = 0;   // the first P*NB items come in one batch (fills the ring without round trips)\n"
        << "    unsigned pf[PREF];\n"
@@ -1341,6 +1345,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                                         : "      nxt = atomicAdd(p.sched + tcur * CS, 1u);\n")
        << "    }\n"
        << "    (void)raw;\n"
+       << "    if (early) pdl_wait();\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
        << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
        << (L.BW > 1 ? "    int bq[" + std::to_string(PQ) + "], eq[" + std::to_string(PQ) + "], nq[" + std::to_string(PQ) +
