@@ -1345,6 +1345,21 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                                         : "      nxt = atomicAdd(p.sched + tcur * CS, 1u);\n")
        << "    }\n"
        << "    (void)raw;\n"
+       << (env_int("O1D_L2PF", 0)
+               ? "    if (early && lane == 0) {\n"
+                 "      // L2 prefetch of the first planes while the preceding kernel drains: a prefetch only\n"
+                 "      // warms L2 (coherent), the shared-memory loads still wait for griddepcontrol.wait\n"
+                 "      for (int k = 0; k < P_NB; ++k) {\n"
+                 "        if (lo + k >= (unsigned)COUNT[tcur]) break;\n"
+                 "        int t3, c3, n3; item_cn((tcur << 22) | (int)(lo + k), t3, c3, n3);\n"
+                 "        asm volatile(\"cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\"\n"
+                 "                     :: \"l\"(&p.in_map[0]), \"r\"(0), \"r\"(0), \"r\"(c3), \"r\"(n3) : \"memory\");\n" +
+                     std::string(wgrad ? "        asm volatile(\"cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\"\n"
+                                         "                     :: \"l\"(&p.out_map), \"r\"(0), \"r\"(0), \"r\"(c3), \"r\"(n3) : \"memory\");\n"
+                                       : "") +
+                 "      }\n"
+                 "    }\n"
+               : "")
        << "    if (early) pdl_wait();\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
        << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
