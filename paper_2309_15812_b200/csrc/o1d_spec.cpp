@@ -1920,7 +1920,11 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
         const int wgm = env_int("O1D_WG_FFMA2", 2);  // 2: pixel pairs (default), 1: dy pairs, 0: scalar
         if (wgm) {
             if (wgm == 2) {
-                const std::pair<int, int> st = pp_step(g, ds);
+                std::pair<int, int> st = pp_step(g, ds);
+                if (env_int("O1D_PPSTEP", -1) >= 0) {  // experiment: force one pairing step for every table
+                    const int f = env_int("O1D_PPSTEP", 0);
+                    st = f == 0 ? std::make_pair(0, 1) : f == 1 ? std::make_pair(1, 0) : f == 2 ? std::make_pair(-1, 1) : std::make_pair(1, 1);
+                }
                 emit_wgrad_compute_pp(os, g, ds, st.first, st.second, "      ", g_chunks);
             }
             else emit_wgrad_compute_runs(os, g, ds, run_axis(g), "      ", g_chunks);
