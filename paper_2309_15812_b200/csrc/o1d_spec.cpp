@@ -1967,6 +1967,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
        << "  __shared__ double part[8][64];\n"
        << "  pdl_wait();\n"
+       << (env_int("O1D_FIN_TRIGGER", 1) ? "  pdl_trigger();   // the next kernel may start its set-up (it waits for our completion)\n" : "")
        << "  const int c = blockIdx.x, j = threadIdx.x >> 5 /* 0..7 */, lane = threadIdx.x & 31;\n"
        << "  const float* base = ws + (u64)c * " << NE << " * " << x.K << ";\n"
        << "  for (int k = lane; k < " << x.K << "; k += 32) {\n"
@@ -2228,6 +2229,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
     os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW) {\n"
        << "  __shared__ double part[8][64];\n"
        << "  pdl_wait();\n"
+       << (env_int("O1D_FIN_TRIGGER", 1) ? "  pdl_trigger();   // the next kernel may start its set-up (it waits for our completion)\n" : "")
        << "  const int c = blockIdx.x, j = threadIdx.x >> 5 /* 0..7 */, lane = threadIdx.x & 31;\n"
        << "  const float* base = ws + (u64)c * " << NE << " * " << x.K << ";\n"
        << "  for (int k = lane; k < " << x.K << "; k += 32) {\n"
