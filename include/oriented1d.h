@@ -165,7 +165,11 @@ O1D_API o1d_status o1d_backward_weight(const o1d_plan *plan, const void *x, cons
 /* One training step of the layer through HOST buffers (the end-to-end path):
  * copies x, w, dy host->device, runs forward, backward_input and
  * backward_weight, copies y, dx, dW device->host, then synchronises `stream`.
- * The plan's internal second stream overlaps the two PCIe directions with each
+ * When all three passes run on the v2 specialised kernels the step is pipelined
+ * over batch chunks (default 8, env O1D_E2E_CHUNKS): the plan's internal streams
+ * copy chunk i+1 in and chunk i-1 out while chunk i is computed (the kernels
+ * take a batch window; dW is finalised once, bitwise equal to the device path).
+ * Otherwise the plan's second stream overlaps the two PCIe directions with each
  * other and with the kernels (forward + D2H y on `stream`; H2D dy,
  * backward_input, D2H dx, backward_weight, D2H dW on the second stream); calls
  * on one plan must not run concurrently.  Host buffers should be pinned.  dev_ws: device scratch of >= o1d_step_host_workspace_bytes(plan)

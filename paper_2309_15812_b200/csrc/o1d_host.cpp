@@ -19,6 +19,11 @@ namespace o1d {
 
 static thread_local std::string g_err;
 
+static int env_int_host(const char *n, int dflt) {
+    const char *v = getenv(n);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
 void set_error(const std::string &msg) { g_err = msg; }
 o1d_status fail(o1d_status st, const std::string &msg) {
     g_err = msg;
@@ -307,6 +312,18 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
         pl->aux_stream = s2;
         pl->aux_ev[0] = e0;
         pl->aux_ev[1] = e1;
+        cudaStream_t s3 = nullptr;
+        bool ok = cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking) == cudaSuccess;
+        pl->aux_stream2 = s3;
+        for (int i = 0; ok && i < o1d_plan::kChunkEv; ++i) {
+            cudaEvent_t e = nullptr;
+            ok = cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+            pl->chunk_ev[i] = e;
+        }
+        if (!ok) {
+            o1d_plan_destroy(pl);
+            return fail(O1D_CUDA_ERROR, "stream/event creation failed");
+        }
     }
     pl->ws_bytes = sizeof(float) * (size_t)d->N * C * pl->bw_bands * K;
     char buf[256];
@@ -328,6 +345,9 @@ void o1d_plan_destroy(o1d_plan *pl) {
     if (!pl) return;
     spec_destroy(pl);
     if (pl->aux_stream) cudaStreamDestroy(static_cast<cudaStream_t>(pl->aux_stream));
+    if (pl->aux_stream2) cudaStreamDestroy(static_cast<cudaStream_t>(pl->aux_stream2));
+    for (void *e : pl->chunk_ev)
+        if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
     for (void *e : pl->aux_ev)
         if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
     if (pl->d_block) cudaFree(pl->d_block);
@@ -439,6 +459,69 @@ o1d_status o1d_step_host(const o1d_plan *pl, const void *x_h, const float *w_h, 
     float *w = reinterpret_cast<float *>(b); b += align256(nw);
     float *dW = reinterpret_cast<float *>(b); b += align256(nw);
     void *ws = b;
+    const int nch = pl->spec && spec_window_ok(pl) && pl->d.N >= 2 && env_int_host("O1D_E2E_CHUNKS", 8) > 1
+                        ? std::min(std::min(pl->d.N, env_int_host("O1D_E2E_CHUNKS", 8)), 16)
+                        : 0;
+    if (nch > 1) {
+        // Pipelined over batch chunks (the kernels take a batch window, so no sub-plans and the
+        // dW partials land in the full workspace: dW is bitwise that of the unchunked step):
+        //   s2 (H2D): w, then per chunk x_i -> ev x_i, dy_i -> ev dy_i
+        //   s  (compute): per chunk: wait x_i: forward_i; wait dy_i: backward_input_i,
+        //                 backward_weight_i (no finalize) -> ev out_i; then the finalize, D2H dW
+        //   s3 (D2H): per chunk: wait out_i: y_i, dx_i
+        // so the two PCIe directions stream concurrently and the kernels fill the gaps.
+        cudaStream_t s = static_cast<cudaStream_t>(stream), s2 = static_cast<cudaStream_t>(pl->aux_stream),
+                     s3 = static_cast<cudaStream_t>(pl->aux_stream2);
+        cudaEvent_t e0 = static_cast<cudaEvent_t>(pl->aux_ev[0]), e1 = static_cast<cudaEvent_t>(pl->aux_ev[1]);
+        auto cu = [](cudaError_t e, const char *what) -> o1d_status {
+            if (e != cudaSuccess) return fail(O1D_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+            return O1D_OK;
+        };
+        auto ev = [&](int kind, int i) { return static_cast<cudaEvent_t>(pl->chunk_ev[kind * 16 + i]); };
+        const size_t px = (size_t)pl->d.C * pl->d.H * pl->d.W * es, py = (size_t)pl->d.C * pl->P * pl->Q * es;
+        if (o1d_status st = cu(cudaEventRecord(e0, s), "event")) return st;  // after prior work on s
+        if (o1d_status st = cu(cudaStreamWaitEvent(s2, e0, 0), "wait")) return st;
+        if (o1d_status st = cu(cudaStreamWaitEvent(s3, e0, 0), "wait")) return st;
+        if (o1d_status st = cu(cudaMemcpyAsync(w, w_h, nw, cudaMemcpyHostToDevice, s2), "H2D w")) return st;
+        int n0s[16], nls[16];
+        for (int i = 0, n0 = 0; i < nch; ++i) {
+            const int nl = pl->d.N / nch + (i < pl->d.N % nch ? 1 : 0);
+            n0s[i] = n0, nls[i] = nl, n0 += nl;
+        }
+        for (int i = 0; i < nch; ++i) {
+            const size_t ox = (size_t)n0s[i] * px, oy = (size_t)n0s[i] * py;
+            if (o1d_status st = cu(cudaMemcpyAsync(static_cast<char *>(x) + ox, static_cast<const char *>(x_h) + ox,
+                                                   (size_t)nls[i] * px, cudaMemcpyHostToDevice, s2), "H2D x"))
+                return st;
+            if (o1d_status st = cu(cudaEventRecord(ev(0, i), s2), "event")) return st;
+            if (o1d_status st = cu(cudaMemcpyAsync(static_cast<char *>(dy) + oy, static_cast<const char *>(dy_h) + oy,
+                                                   (size_t)nls[i] * py, cudaMemcpyHostToDevice, s2), "H2D dy"))
+                return st;
+            if (o1d_status st = cu(cudaEventRecord(ev(1, i), s2), "event")) return st;
+        }
+        for (int i = 0; i < nch; ++i) {
+            if (o1d_status st = cu(cudaStreamWaitEvent(s, ev(0, i), 0), "wait")) return st;
+            if (o1d_status st = spec_run(pl, 0, x, w, y, nullptr, nullptr, s, n0s[i], nls[i], true)) return st;
+            if (o1d_status st = cu(cudaStreamWaitEvent(s, ev(1, i), 0), "wait")) return st;
+            if (o1d_status st = spec_run(pl, 1, dy, w, dx, nullptr, nullptr, s, n0s[i], nls[i], true)) return st;
+            if (o1d_status st = spec_run(pl, 2, x, nullptr, dy, dW, static_cast<float *>(ws), s, n0s[i], nls[i], false))
+                return st;
+            if (o1d_status st = cu(cudaEventRecord(ev(2, i), s), "event")) return st;
+            const size_t ox = (size_t)n0s[i] * px, oy = (size_t)n0s[i] * py;
+            if (o1d_status st = cu(cudaStreamWaitEvent(s3, ev(2, i), 0), "wait")) return st;
+            if (o1d_status st = cu(cudaMemcpyAsync(static_cast<char *>(y_h) + oy, static_cast<char *>(y) + oy,
+                                                   (size_t)nls[i] * py, cudaMemcpyDeviceToHost, s3), "D2H y"))
+                return st;
+            if (o1d_status st = cu(cudaMemcpyAsync(static_cast<char *>(dx_h) + ox, static_cast<char *>(dx) + ox,
+                                                   (size_t)nls[i] * px, cudaMemcpyDeviceToHost, s3), "D2H dx"))
+                return st;
+        }
+        if (o1d_status st = spec_finalize(pl, dW, static_cast<float *>(ws), s)) return st;
+        if (o1d_status st = cu(cudaMemcpyAsync(dW_h, dW, nw, cudaMemcpyDeviceToHost, s), "D2H dW")) return st;
+        if (o1d_status st = cu(cudaEventRecord(e1, s3), "event")) return st;
+        if (o1d_status st = cu(cudaStreamWaitEvent(s, e1, 0), "wait")) return st;
+        return cu(cudaStreamSynchronize(s), "o1d_step_host");
+    }
     // Two streams so the PCIe directions overlap with each other and with the
     // kernels:  s  : H2D w, x  -> forward        -> D2H y
     //           s2 : H2D dy    -> backward_input -> D2H dx -> (x ready) backward_weight -> D2H dW

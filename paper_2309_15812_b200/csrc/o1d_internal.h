@@ -56,6 +56,9 @@ struct o1d_plan {
     o1d::SpecSet *spec = nullptr;     // null => generic kernels only
     void *aux_stream = nullptr;       // o1d_step_host's second stream (cudaStream_t)
     void *aux_ev[2] = {nullptr, nullptr};
+    void *aux_stream2 = nullptr;      // o1d_step_host's third stream (device -> host copies, pipelined path)
+    static constexpr int kChunkEv = 3 * 16;
+    void *chunk_ev[kChunkEv] = {};    // per batch chunk: inputs on device x / dy, outputs ready
     std::string describe;
 };
 

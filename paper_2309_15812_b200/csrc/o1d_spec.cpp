@@ -268,6 +268,7 @@ struct Params {
   int adapt;         // 1: this launch measures per-table costs and updates the placement (every K-th launch)
   u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
   void* bal;         // v2 adaptive balance state (Bal) or null
+  int n0, nlen;      // v2 batch window: planes with n in [n0, n0 + nlen) (nlen = 0: the whole batch)
 };
 // Adaptive placement (v2): consumers add their per-item busy cycles per table; the
 // last consumer warp of a launch turns them into per-table costs (blended with the
@@ -364,9 +365,12 @@ __device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
 // specialised code path in the instruction cache) and moves on to the next
 // table when it is exhausted.  `raw` is a counter value fetched one plane
 // ahead, so the atomic's latency is hidden behind a whole plane of compute.
-__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried, bool steal) {
+// items of table t in this launch: all of it, or (CMAJOR item order) the planes of the
+// batch window -- a contiguous item range nch * [0, nlen), shifted by n0 in item_cn
+__device__ __forceinline__ int cnt_w(int t, int nlen) { return nlen > 0 ? (CHOFF[t + 1] - CHOFF[t]) * nlen : COUNT[t]; }
+__device__ __forceinline__ int sched_resolve(unsigned* sched, int& tcur, unsigned& raw, int& tried, bool steal, int nlen = 0) {
   while (tcur >= 0) {
-    if (raw < (unsigned)COUNT[tcur]) return (tcur << 22) | (int)raw;
+    if (raw < (unsigned)cnt_w(tcur, nlen)) return (tcur << 22) | (int)raw;
     if (++tried >= NT || !STEAL || !steal) { tcur = -1; break; }
     tcur = tcur + 1 == NT ? 0 : tcur + 1;
     raw = atomicAdd(sched + tcur * CS, 1u);
@@ -392,7 +396,7 @@ __device__ __forceinline__ int sched2_next(unsigned* sched, int& tcur, unsigned&
 __device__ __forceinline__ void sched_prefetch(unsigned* sched, int tcur, unsigned& raw) {
   if (tcur >= 0) raw = atomicAdd(sched + tcur * CS, 1u);
 }
-__device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
+__device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n, int n0 = 0) {
   t = (item >> 22) & 31;   // bits 27..29: batch flags (v2 wgrad)
   const int i = item & 0x3FFFFF;
 #if CMAJOR
@@ -401,6 +405,7 @@ __device__ __forceinline__ void item_cn(int item, int& t, int& c, int& n) {
   const int nch = CHOFF[t + 1] - CHOFF[t];
   n = i / nch;
   c = CHLIST[CHOFF[t] + (i - n * nch)];
+  n += n0;
 #else
   c = CHLIST[CHOFF[t] + i / NB];
   n = i - (i / NB) * NB;
@@ -1350,8 +1355,8 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                  "      // L2 prefetch of the first planes while the preceding kernel drains: a prefetch only\n"
                  "      // warms L2 (coherent), the shared-memory loads still wait for griddepcontrol.wait\n"
                  "      for (int k = 0; k < P_NB; ++k) {\n"
-                 "        if (lo + k >= (unsigned)COUNT[tcur]) break;\n"
-                 "        int t3, c3, n3; item_cn((tcur << 22) | (int)(lo + k), t3, c3, n3);\n"
+                 "        if (lo + k >= (unsigned)cnt_w(tcur, p.nlen)) break;\n"
+                 "        int t3, c3, n3; item_cn((tcur << 22) | (int)(lo + k), t3, c3, n3, p.n0);\n"
                  "        asm volatile(\"cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\"\n"
                  "                     :: \"l\"(&p.in_map[0]), \"r\"(0), \"r\"(0), \"r\"(c3), \"r\"(n3) : \"memory\");\n" +
                      std::string(wgrad ? "        asm volatile(\"cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\"\n"
@@ -1392,13 +1397,13 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << (env_int("O1D_PREF", 2) > 1 && !env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) {\n"
                  "          // PREF single-item atomics in flight: each issue consumes the oldest one\n"
-                 "          if (fetched < P_NB && lo + fetched < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + fetched);\n"
+                 "          if (fetched < P_NB && lo + fetched < (unsigned)cnt_w(tcur, p.nlen)) item = (tcur << 22) | (int)(lo + fetched);\n"
                  "          else {\n"
                  "            unsigned v = pf[0];\n"
                  "#pragma unroll\n"
                  "            for (int k = 0; k + 1 < PREF; ++k) pf[k] = pf[k + 1];\n"
                  "            const int t0 = tcur;\n"
-                 "            item = sched_resolve(p.sched, tcur, v, tried, p.only < 0);\n"
+                 "            item = sched_resolve(p.sched, tcur, v, tried, p.only < 0, p.nlen);\n"
                  "            if (tcur != t0) {   // moved to another table: the prefetched indices belong to the old one\n"
                  "#pragma unroll\n"
                  "              for (int k = 0; k < PREF; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
@@ -1411,8 +1416,8 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                : env_int("O1D_SCHED2", 0)
                ? "        if (lane == 0) item = sched2_next(p.sched, tcur, lo, hi, nxt, tried, p.only < 0);\n"
                : "        if (lane == 0) {\n"
-                 "          if (fetched < P_NB && lo + fetched < (unsigned)COUNT[tcur]) item = (tcur << 22) | (int)(lo + fetched);\n"
-                 "          else { item = sched_resolve(p.sched, tcur, nxt, tried, p.only < 0); sched_prefetch(p.sched, tcur, nxt); }\n"
+                 "          if (fetched < P_NB && lo + fetched < (unsigned)cnt_w(tcur, p.nlen)) item = (tcur << 22) | (int)(lo + fetched);\n"
+                 "          else { item = sched_resolve(p.sched, tcur, nxt, tried, p.only < 0, p.nlen); sched_prefetch(p.sched, tcur, nxt); }\n"
                  "          ++fetched;\n"
                  "        }\n")
        << (L.BW > 1 ? "          bq[qi] = __shfl_sync(0xffffffffu, item, 0); eq[qi] = 0;\n"
@@ -1433,7 +1438,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "        item = __shfl_sync(0xffffffffu, item, 0);\n"
        << "        ++issued;\n"
        << "        int t2 = 0, c2 = 0, n2 = 0;\n"
-       << "        if (item >= 0) item_cn(item, t2, c2, n2);\n"
+       << "        if (item >= 0) item_cn(item, t2, c2, n2, p.n0);\n"
        << "        if (lane == 0) {\n"
        << "          s_item[s] = item;\n"
        << "          if (item >= 0) {\n"
@@ -1500,7 +1505,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     "      item = s_item[s];\n" \
     "      if (lane == 0) trace_ev(p.trace, 3, item, trn);\n" \
     "      if (item < 0) break;\n" \
-    "      item_cn(item, t, c, n);\n" \
+    "      item_cn(item, t, c, n, p.n0);\n" \
     "    }\n"
 
 // adaptive placement accounting (per consumer warp): busy cycles per item of table t
@@ -2599,6 +2604,32 @@ void spec_destroy(o1d_plan *pl) {
 }
 
 bool spec_has(const o1d_plan *pl, int pass) { return pl->spec && pass >= 0 && pass < 3; }
+// batch windows (o1d_step_host pipelining): every pass on the v2 kernels with the default
+// channel-major item order, single-plane wgrad items and the default scheduler
+bool spec_window_ok(const o1d_plan *pl) {
+    const SpecSet *sp = pl->spec;
+    return sp && sp->v2p[0] && sp->v2p[1] && sp->v2p[2] && env_int("O1D_CMAJOR", 1) && env_int("O1D_WB", 1) == 1 &&
+           !env_int("O1D_SCHED2", 0) && !env_int("O1D_SEQ", 0);
+}
+o1d_status spec_finalize(const o1d_plan *pl, float *dW, const float *ws, void *stream) {
+    const SpecSet *sp = pl->spec;
+    const void *wsp = ws;
+    void *fargs[] = {&wsp, &dW};
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig fc{};
+    fc.gridDimX = (unsigned)pl->d.C;
+    fc.gridDimY = fc.gridDimZ = 1;
+    fc.blockDimX = 256;
+    fc.blockDimY = fc.blockDimZ = 1;
+    fc.hStream = static_cast<CUstream>(stream);
+    fc.attrs = attr;
+    fc.numAttrs = env_int("O1D_PDL", 1) != 0 ? 1 : 0;
+    const CUresult r = drv().launchKernelEx(&fc, sp->fin, fargs, nullptr);
+    if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of wgrad finalize: " + cu_err(r));
+    return O1D_OK;
+}
 int spec_launches(const o1d_plan *, int pass) { return pass == 2 ? 2 : 1; }
 size_t spec_workspace_bytes(const o1d_plan *pl) {
     if (!pl->spec) return 0;
@@ -2606,11 +2637,12 @@ size_t spec_workspace_bytes(const o1d_plan *pl) {
 }
 
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW, float *ws,
-                    void *stream) {
+                    void *stream, int n0, int nlen, bool finalize) {
+    if (nlen > 0 && !spec_window_ok(pl)) return fail(O1D_UNSUPPORTED, "batch windows need the v2 kernels");
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const int nt = sp->nt;
-    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 10 * sizeof(void *)];
+    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 11 * sizeof(void *)];
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(blob);
     const std::vector<Geo> &geo = pass == 1 ? sp->bwd : sp->fwd;
     // input maps (x for forward / wgrad, dy for backward_input), one box per table
@@ -2645,6 +2677,9 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     }
     ptrs[7] = sp->d_trace;
     ptrs[8] = (sp->d_bal && sp->v2p[pass] && sp->home2[pass].size() > 0) ? sp->d_bal + (size_t)pass * kBalBytes : nullptr;
+    int *win = reinterpret_cast<int *>(ptrs + 9);
+    win[0] = nlen > 0 ? n0 : 0;
+    win[1] = nlen > 0 ? nlen : 0;
     void *args[] = {blob};
     CUlaunchAttribute attr[1];
     attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -2686,7 +2721,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
         r = drv().launchKernelEx(&cfg, sp->fn[pass], args, nullptr);
     }
     if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, "launch of specialised kernel: " + cu_err(r));
-    if (pass == 2) {
+    if (pass == 2 && finalize) {
         const void *wsp = ws;
         void *fargs[] = {&wsp, &dW};
         CUlaunchConfig fc = cfg;

@@ -295,3 +295,24 @@ def test_1dpp_block_workloads(which):
     wl = inputs.WORKLOADS[which]
     run_case(4, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, torch.float32, 0,
              check_det=True)
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "8"])
+def test_step_host_pipelined_bitwise(chunks, monkeypatch):
+    """o1d_step_host pipelined over batch chunks (v2 kernels with a batch window; H2D,
+    kernels and D2H on three streams) gives bitwise the device path's y, dx and dW
+    (the chunks' dW partials land in the full workspace; one finalize)."""
+    monkeypatch.setenv("O1D_E2E_CHUNKS", chunks)
+    angles = T.direction_angles(8, 16, "cycled")
+    plan = B.Plan(8, 16, 56, 56, 31, np.array(angles), device="cuda:0")
+    assert "spec-v2" in plan.describe()
+    x = torch.from_numpy(inputs.activation(plan.x_shape(), 0)).pin_memory()
+    w = torch.from_numpy(inputs.weights(16, 31)).pin_memory()
+    dy = torch.from_numpy(inputs.activation(plan.y_shape(), 2)).pin_memory()
+    y, dx, dW = torch.empty_like(x).pin_memory(), torch.empty_like(x).pin_memory(), torch.empty_like(w).pin_memory()
+    for _ in range(2):
+        B.step_host(plan, x, w, dy, y, dx, dW, B.step_host_workspace(plan))
+        xd, wd, dyd = x.cuda(), w.cuda(), dy.cuda()
+        assert torch.equal(y, B.forward(plan, xd, wd).cpu())
+        assert torch.equal(dx, B.backward_input(plan, dyd, wd).cpu())
+        assert torch.equal(dW, B.backward_weight(plan, xd, dyd).cpu())
