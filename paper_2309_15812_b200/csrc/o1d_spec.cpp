@@ -656,6 +656,7 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
 int g_chunks = 0;
 #define EFH (env_int("O1D_EF", 1) != 0)  // evict-first L2 hints on the streaming TMA traffic (v2)
 #define YST (env_int("O1D_YSTORE", 0) != 0)  // stencil outputs by warp copy instead of TMA band store
+#define YSTG (env_int("O1D_YSTG", 0) != 0)   // stencil outputs stored from registers (no staging band)
 struct Chunker {
     std::ostringstream &os;
     const char *ind;
@@ -1279,7 +1280,7 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.off_w = L.off_bal + 16 * 8 + 16 * 4 + 16;
     L.off_scr = L.off_w + (wgrad ? 0 : (size_t)NSmax * 64 * 4);
     L.off_stg = (L.off_scr + (wgrad ? (size_t)L.ncw() * 32 * 4 : 0) + 127) & ~(size_t)127;
-    L.sb = wgrad ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
+    L.sb = (wgrad || YSTG) ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
     L.off_dy = L.off_stg + (size_t)L.ncw() * L.sb;
     L.off_t = (L.off_dy + (size_t)L.P * L.db + 1023) & ~(size_t)1023;
     const size_t budget = (size_t)env_int("O1D_SMEM_KB", 227) * 1024 - 64;
@@ -1573,7 +1574,27 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     os << "    }\n"
        << "    if (warm) continue;\n"
        << "    __syncwarp();\n"
-       << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n"
+       << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n";
+    if (YSTG) {  // O1D_YSTG=1: outputs straight from registers (streaming stores), no staging band
+        os << "    if (active) {\n"
+           << "      act_t* const yo = reinterpret_cast<act_t*>(p.io) + ((u64)(n * " << x.C << " + c) * " << x.Ho << " + " << R
+           << " * br) * " << x.Wo << " + " << S << " * bc;\n";
+        for (int r = 0; r < R; ++r)
+            for (int s2 = 0; s2 < S; ++s2) {
+                os << "      ";
+                if (ragged) os << "if (" << R << " * br + " << r << " < " << x.Ho << " && " << S << " * bc + " << s2 << " < " << x.Wo << ") ";
+                os << "__stcs(yo + " << r * x.Wo + s2 << ", to_act(a" << r << "_" << s2 << "));\n";
+            }
+        os << "    }\n"
+           << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+           << BAL_ITEM_END
+           << "  }\n"
+           << BAL_EXIT
+           << "}\n";
+        g_chunks = 0;
+        return os.str();
+    }
+    os << ""
        << (YST ? "" : "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n")
        << "    __syncwarp();\n"
        << "    if (active) {\n"
