@@ -592,7 +592,7 @@ int range_cost(const Geo &g, int lo, int hi) {
 // meet at the output combine, so the slowest group sets the pace).
 int pair_axis(const Geo &g);
 int parity_of(int v);
-bool g_parity_groups = true;  // set per plan (O1D_PARITY)
+thread_local bool g_parity_groups = true;  // set per plan (O1D_PARITY)
 
 std::vector<int> group_taps(const Geo &g, int gi, int G) {
     const int nd = (int)g.taps.size();
@@ -653,7 +653,7 @@ void for_each_pixel(const Geo &g, const std::vector<int> &ds, F &&f) {
 // (wm = ~0), the warm-up pass at kernel start runs one chunk per consumer warp so
 // the cold code is fetched by all warps in parallel (measured: the first tap loop
 // of a table otherwise takes ~10 us of instruction fetch instead of ~1.6 us).
-int g_chunks = 0;
+thread_local int g_chunks = 0;  // (generator state: plans may be created from several threads)
 #define EFH (env_int("O1D_EF", 1) != 0)  // evict-first L2 hints on the streaming TMA traffic (v2)
 #define YST (env_int("O1D_YSTORE", 0) != 0)  // stencil outputs by warp copy instead of TMA band store
 #define YSTG (env_int("O1D_YSTG", 0) != 0)   // stencil outputs stored from registers (no staging band)
