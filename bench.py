@@ -44,9 +44,10 @@ def parse():
                     help="give every channel this single angle (per-angle uniformity runs) instead of D=8")
     ap.add_argument("--dirs", type=int, default=None, help="number of directions D (default: the workload's 8)")
     ap.add_argument("--K", type=int, default=None, help="kernel length (experiments; default: the workload's 31)")
-    ap.add_argument("--workload", default="s1", choices=["s1", "pp_main", "pp_res"],
+    ap.add_argument("--workload", default="s1", choices=["s1", "pp_main", "pp_res", "ks"],
                     help="s1 = BASELINE configs[1] (default); pp_main / pp_res = the 1D++ block's K=15 main and "
-                         "C=384 residual oriented convs (SURVEY NEXT-3)")
+                         "C=384 residual oriented convs (SURVEY NEXT-3); ks = configs[2], the kernel-length sweep "
+                         "(N=128, C=384, 14x14, K from --K) with a KxK depthwise conv2d comparator")
     ap.add_argument("--disc", default="rotation", choices=["rotation", "shear"],
                     help="tap discretisation: rotation (Def. 1) or shear (Appendix, P:386-440)")
     ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
@@ -282,7 +283,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.dtype]
     es = 4 if args.dtype == "f32" else 2
-    wl = inputs.WORKLOADS[args.workload]
+    wl = inputs.ksweep(args.K or 31) if args.workload == "ks" else inputs.WORKLOADS[args.workload]
     if args.dirs is not None:
         from dataclasses import replace
         wl = replace(wl, D=args.dirs)
@@ -396,6 +397,28 @@ def run_ours(args):
         extra["fp32_tflops_dense"] = 3 * 2 * algorithmic_fmas(wl) / (ms_step * 1e-3) / 1e12
         extra["imgs_per_s_layer_step"] = wl.N * world / (ms_step * 1e-3)
         extra["plan"] = plan.describe()
+        if args.workload == "ks":
+            # configs[2] "vs equivalent kxk depthwise (linear-cost check)": torch conv2d (cuDNN),
+            # groups=C, K x K, same activations, forward + both gradients -- a library comparator
+            xk = sets[0]["x"].detach().clone().requires_grad_(True)
+            wk = torch.randn(wl.C, 1, wl.K, wl.K, device=dev, dtype=tdt, requires_grad=True)
+            gk = sets[0]["dy"]
+            def kxk():
+                yk = torch.nn.functional.conv2d(xk, wk, padding=wl.K // 2, groups=wl.C)
+                yk.backward(gk)
+            for _ in range(3):
+                kxk()
+            torch.cuda.synchronize()
+            t0k, t1k = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nk = 10
+            t0k.record(stream)
+            for _ in range(nk):
+                kxk()
+            t1k.record(stream)
+            torch.cuda.synchronize()
+            extra["comparator"] = {"what": f"torch conv2d depthwise {wl.K}x{wl.K} fwd+bwd (cuDNN), same shape",
+                                   "ms_per_step": t0k.elapsed_time(t1k) / nk, "ours_ms_per_step": ms_step,
+                                   "ours_speedup": (t0k.elapsed_time(t1k) / nk) / ms_step}
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
