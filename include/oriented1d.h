@@ -179,6 +179,16 @@ O1D_API o1d_status o1d_step_host(const o1d_plan *plan, const void *x_h, const fl
                          void *y_h, void *dx_h, float *dW_h, void *dev_ws, size_t dev_ws_bytes,
                          void *stream);
 
+/* One training step of the layer on device buffers: forward (x -> y), backward_input
+ * (dy -> dx) and backward_weight ((x, dy) -> dW), the same results as the three
+ * calls in that order (bitwise).  The passes read only the step's inputs and write
+ * disjoint outputs, so on the specialised kernels the second and third pass skip the
+ * wait for the preceding pass and overlap its tail (programmatic dependent launch);
+ * the first waits for the work before it on `stream`.  Buffers as for the three
+ * calls; ws: >= o1d_workspace_bytes(plan).  Outputs must not alias inputs. */
+O1D_API o1d_status o1d_step(const o1d_plan *plan, const void *x, const float *w, const void *dy, void *y, void *dx,
+                            float *dW, void *ws, size_t ws_bytes, void *stream);
+
 /* Number of kernel launches one call of each pass issues (for launch accounting). */
 O1D_API int32_t o1d_launches_per_call(const o1d_plan *plan, int32_t pass /* 0 fwd, 1 bwd_in, 2 bwd_w */);
 

@@ -32,7 +32,7 @@ EXPORTS = ["o1d_make_taps", "o1d_direction_angles", "o1d_plan_create", "o1d_plan
            "o1d_plan_get_taps", "o1d_plan_describe", "o1d_workspace_bytes", "o1d_forward",
            "o1d_backward_input", "o1d_backward_weight", "o1d_step_host_workspace_bytes", "o1d_step_host",
            "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source",
-           "o1d_debug_trace", "o1d_make_taps_ex"]
+           "o1d_debug_trace", "o1d_make_taps_ex", "o1d_step"]
 
 
 class O1DError(RuntimeError):
@@ -78,6 +78,7 @@ def lib():
                 "o1d_version": (ctypes.c_char_p, []),
                 "o1d_debug_trace": (ctypes.c_size_t, [vp, vp, ctypes.c_size_t]),
                 "o1d_make_taps_ex": (st, [i32, i32, i32, f64p, i32, i16p, i16p]),
+                "o1d_step": (st, [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
                 "o1d_spec_source": (st, [ctypes.POINTER(_Desc), f64p, i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
             }
             for name, (res, args) in sig.items():
@@ -260,6 +261,24 @@ def backward_weight(plan: Plan, x, dy, dW=None, ws=None, stream=None):
     _check(lib().o1d_backward_weight(plan.handle, x.data_ptr(), dy.data_ptr(), dW.data_ptr(), ws.data_ptr(),
                                      ws.numel() * ws.element_size(), _stream_handle(stream)))
     return dW
+
+
+def step(plan: Plan, x, w, dy, y=None, dx=None, dW=None, ws=None, stream=None):
+    """One layer training step on device tensors (o1d_step): forward, backward_input and
+    backward_weight with the later passes overlapping the earlier ones' tails."""
+    _check_tensor(x, "x", plan.x_shape(), plan.dtype, plan.device)
+    _check_tensor(dy, "dy", plan.y_shape(), plan.dtype, plan.device)
+    _check_tensor(w, "w", (plan.C, plan.K), torch.float32, plan.device)
+    y = torch.empty(plan.y_shape(), dtype=plan.dtype, device=plan.device) if y is None else y
+    dx = torch.empty(plan.x_shape(), dtype=plan.dtype, device=plan.device) if dx is None else dx
+    dW = torch.empty((plan.C, plan.K), dtype=torch.float32, device=plan.device) if dW is None else dW
+    _check_tensor(y, "y", plan.y_shape(), plan.dtype, plan.device)
+    _check_tensor(dx, "dx", plan.x_shape(), plan.dtype, plan.device)
+    _check_tensor(dW, "dW", (plan.C, plan.K), torch.float32, plan.device)
+    ws = workspace(plan) if ws is None else ws
+    _check(lib().o1d_step(plan.handle, x.data_ptr(), w.data_ptr(), dy.data_ptr(), y.data_ptr(), dx.data_ptr(),
+                          dW.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(), _stream_handle(stream)))
+    return y, dx, dW
 
 
 def step_host_workspace(plan: Plan):

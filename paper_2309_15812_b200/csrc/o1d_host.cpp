@@ -423,6 +423,27 @@ o1d_status o1d_backward_weight(const o1d_plan *pl, const void *x, const void *dy
     return generic_bwd_weight(pl, x, dy, dW, static_cast<float *>(ws), stream);
 }
 
+o1d_status o1d_step(const o1d_plan *pl, const void *x, const float *w, const void *dy, void *y, void *dx, float *dW,
+                    void *ws, size_t ws_bytes, void *stream) {
+    if (!pl) return fail(O1D_INVALID_ARG, "NULL plan");
+    for (const void *q : {x, (const void *)w, dy, (const void *)y, (const void *)dx, (const void *)dW, (const void *)ws})
+        if (o1d_status st = check_ptr(q, "o1d_step buffer")) return st;
+    if (ws_bytes < o1d_workspace_bytes(pl)) return fail(O1D_WORKSPACE_TOO_SMALL, "ws_bytes < o1d_workspace_bytes(plan)");
+    if (o1d_status st = check_device(pl)) return st;
+    if (!(pl->spec && spec_has(pl, 0) && spec_has(pl, 1) && spec_has(pl, 2))) {
+        if (o1d_status st = o1d_forward(pl, x, w, y, stream)) return st;
+        if (o1d_status st = o1d_backward_input(pl, dy, w, dx, stream)) return st;
+        return o1d_backward_weight(pl, x, dy, dW, ws, ws_bytes, stream);
+    }
+    // The three passes of a step read only the step's inputs (x, w, dy) and write disjoint
+    // outputs, so backward_input and backward_weight need not wait for the preceding pass:
+    // they start on the SMs the preceding pass frees (its tail) instead of after it.  The
+    // forward still waits for whatever preceded the step on the stream.
+    if (o1d_status st = spec_run(pl, 0, x, w, y, nullptr, nullptr, stream)) return st;
+    if (o1d_status st = spec_run(pl, 1, dy, w, dx, nullptr, nullptr, stream, 0, 0, true, true)) return st;
+    return spec_run(pl, 2, x, nullptr, dy, dW, static_cast<float *>(ws), stream, 0, 0, true, true);
+}
+
 int32_t o1d_launches_per_call(const o1d_plan *pl, int32_t pass) {
     if (!pl) return 0;
     if (pl->spec && spec_has(pl, pass)) return spec_launches(pl, pass);

@@ -269,6 +269,7 @@ struct Params {
   u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
   void* bal;         // v2 adaptive balance state (Bal) or null
   int n0, nlen;      // v2 batch window: planes with n in [n0, n0 + nlen) (nlen = 0: the whole batch)
+  int nowait;        // 1: no griddepcontrol.wait (the inputs do not come from the preceding kernel, o1d_step)
 };
 // Adaptive placement (v2): consumers add their per-item busy cycles per table; the
 // last consumer warp of a launch turns them into per-table costs (blended with the
@@ -1338,7 +1339,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "    // first atomics run before griddepcontrol.wait, overlapping the preceding kernel's tail\n"
        << "    // (only the data -- x / dy / w -- may be produced by it)\n"
        << "    const bool early = " << (env_int("O1D_EARLY", 1) ? "p.bal == nullptr" : "false") << ";\n"
-       << "    if (!early) pdl_wait();\n"
+       << "    if (!early && !p.nowait) pdl_wait();\n"
        << "    const u64 pol = " << (EFH ? "policy_evict_first()" : "0ull") << ";\n"
        << "    unsigned lo = 0, hi = 0, nxt = 0;   // the first P*NB items come in one batch (fills the ring without round trips)\n"
        << "    unsigned pf[PREF];\n"
@@ -1366,7 +1367,7 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                  "      }\n"
                  "    }\n"
                : "")
-       << "    if (early) pdl_wait();\n"
+       << "    if (early && !p.nowait) pdl_wait();\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
        << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
        << (L.BW > 1 ? "    int bq[" + std::to_string(PQ) + "], eq[" + std::to_string(PQ) + "], nq[" + std::to_string(PQ) +
@@ -2658,12 +2659,12 @@ size_t spec_workspace_bytes(const o1d_plan *pl) {
 }
 
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW, float *ws,
-                    void *stream, int n0, int nlen, bool finalize) {
+                    void *stream, int n0, int nlen, bool finalize, bool nowait) {
     if (nlen > 0 && !spec_window_ok(pl)) return fail(O1D_UNSUPPORTED, "batch windows need the v2 kernels");
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const int nt = sp->nt;
-    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 11 * sizeof(void *)];
+    alignas(64) unsigned char blob[sizeof(CUtensorMap) * 17 + 12 * sizeof(void *)];
     CUtensorMap *maps = reinterpret_cast<CUtensorMap *>(blob);
     const std::vector<Geo> &geo = pass == 1 ? sp->bwd : sp->fwd;
     // input maps (x for forward / wgrad, dy for backward_input), one box per table
@@ -2701,6 +2702,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w,
     int *win = reinterpret_cast<int *>(ptrs + 9);
     win[0] = nlen > 0 ? n0 : 0;
     win[1] = nlen > 0 ? nlen : 0;
+    *reinterpret_cast<int *>(ptrs + 10) = (nowait && sp->v2p[pass]) ? 1 : 0;
     void *args[] = {blob};
     CUlaunchAttribute attr[1];
     attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;

@@ -20,7 +20,7 @@ size_t spec_trace(const o1d_plan *pl, void *host, size_t bytes);
 // n0/nlen: batch window (planes n in [n0, n0 + nlen), nlen = 0: all); finalize: pass 2 also
 // launches the dW finalize (set false for all but the last window, see spec_finalize)
 o1d_status spec_run(const o1d_plan *pl, int pass, const void *a, const float *w, const void *b, float *dW,
-                    float *ws, void *stream, int n0 = 0, int nlen = 0, bool finalize = true);
+                    float *ws, void *stream, int n0 = 0, int nlen = 0, bool finalize = true, bool nowait = false);
 bool spec_window_ok(const o1d_plan *pl);
 o1d_status spec_finalize(const o1d_plan *pl, float *dW, const float *ws, void *stream);
 }  // namespace o1d

@@ -316,3 +316,24 @@ def test_step_host_pipelined_bitwise(chunks, monkeypatch):
         assert torch.equal(y, B.forward(plan, xd, wd).cpu())
         assert torch.equal(dx, B.backward_input(plan, dyd, wd).cpu())
         assert torch.equal(dW, B.backward_weight(plan, xd, dyd).cpu())
+
+
+
+def test_step_api_bitwise_and_repeated():
+    """o1d_step (the three passes with the later ones overlapping the earlier ones' tails)
+    gives bitwise the results of the three separate calls, step after step."""
+    wl = inputs.S1
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, np.array(angles), device="cuda:0")
+    g = torch.Generator(device="cuda:0").manual_seed(1)
+    x = torch.rand(wl.N, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    dy = torch.rand(wl.N, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    w = torch.rand(wl.C, wl.K, device="cuda:0", generator=g)
+    y0, dx0, dW0 = B.forward(plan, x, w), B.backward_input(plan, dy, w), B.backward_weight(plan, x, dy)
+    ws = B.workspace(plan)
+    y, dx, dW = torch.empty_like(y0), torch.empty_like(dx0), torch.empty_like(dW0)
+    for i in range(100):
+        B.step(plan, x, w, dy, y, dx, dW, ws)
+        if i % 25 == 24:
+            torch.cuda.synchronize()
+            assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0), i
