@@ -1475,6 +1475,9 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "      }\n"
        << "      if (!any) { if (++idle > " << env_int("O1D_IDLE", 1) << ") __nanosleep(" << env_int("O1D_SLEEP", 256) << "); } else idle = 0;\n"
        << "    }\n"
+       << "    // a kernel that skipped griddepcontrol.wait (o1d_step) still completes only after its\n"
+       << "    // predecessor: whatever waits for this grid then also sees the predecessor done\n"
+       << "    if (p.nowait) pdl_wait();\n"
        << "    pdl_trigger();\n"
        << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
        << "    return;\n"
