@@ -658,6 +658,9 @@ thread_local int g_chunks = 0;  // (generator state: plans may be created from s
 #define EFH (env_int("O1D_EF", 1) != 0)  // evict-first L2 hints on the streaming TMA traffic (v2)
 #define YST (env_int("O1D_YSTORE", 0) != 0)  // stencil outputs by warp copy instead of TMA band store
 #define YSTG (env_int("O1D_YSTG", 0) != 0)   // stencil outputs stored from registers (no staging band)
+// stencil outputs staged in the consumed tile slot (v2).  Off: measured 48.1 vs 45.2 us forward at
+// P = 4 (pair barrier + deferred slot release), and the extra pair it makes room for (P = 5) was slower still
+#define INSLOT (env_int("O1D_INSLOT", 0) != 0)
 struct Chunker {
     std::ostringstream &os;
     const char *ind;
@@ -1245,13 +1248,15 @@ std::string gen_stencil(const Ctx &x, const std::vector<Geo> &geo, const std::ve
 // ---------------------------------------------------------------------------
 struct Lay2 {
     int NS = 3, NB = 2, P = 1, NPROD = 1, wpg = 1, pitch = 0, zrows = 0, dyp = 0, dyrows = 0, hin = 0, BW = 1;
+    bool inslot = false;   // stencil output bands staged in the consumed slot (no staging area)
+    size_t sbi = 0;        // bytes per warp band inside the slot
     size_t zb = 0, tb = 0, db = 0, sb = 0, off_item = 0, off_bal = 0, off_w = 0, off_scr = 0, off_stg = 0, off_dy = 0, off_t = 0,
            total = 0;
     int ncw() const { return P * wpg; }
     size_t slot(int s) const { return off_t + zb + (size_t)s * (zb + tb); }
 };
 
-Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad) {
+Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad, bool allow_inslot = true) {
     Lay2 L;
     L.wpg = x.wpg;
     L.hin = Hin;
@@ -1260,8 +1265,7 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.BW = wgrad ? std::max(1, std::min(x.N, env_int("O1D_WB", 1))) : 1;  // (measured: 4 -> 58 us vs 51 us, register pressure)
     L.P = std::max(1, std::min(8, env_int("O1D_P", std::max(1, 8 / x.wpg))));
     while (L.P * L.wpg > 15) --L.P;
-    L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", 2)));
-    while (L.P % L.NPROD) --L.NPROD;   // producers serve P / NPROD pairs each
+    L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", 2)));   // producer pw serves pairs pw, pw + NPROD, ...
     for (auto &g : geo) {
         L.pitch = std::max(L.pitch, g.pitch);
         L.zrows = std::max(L.zrows, std::max(-g.minDH, R * x.BR - Hin + g.maxDH) + 1);
@@ -1281,7 +1285,11 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.off_w = L.off_bal + 16 * 8 + 16 * 4 + 16;
     L.off_scr = L.off_w + (wgrad ? 0 : (size_t)NSmax * 64 * 4);
     L.off_stg = (L.off_scr + (wgrad ? (size_t)L.ncw() * 32 * 4 : 0) + 127) & ~(size_t)127;
-    L.sb = (wgrad || YSTG) ? 0 : ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;  // per-warp output staging band
+    L.sbi = ((size_t)4 * R * x.Wo * es + 127) & ~(size_t)127;
+    // O1D_INSLOT: a pair writes its output bands into the slot it just consumed (the slot is
+    // released once the band stores have read it), so the staging area becomes tile slots
+    L.inslot = allow_inslot && INSLOT && !wgrad && !YSTG && !YST && (size_t)L.wpg * L.sbi <= (size_t)Hin * L.pitch * es;
+    L.sb = (wgrad || YSTG || L.inslot) ? 0 : L.sbi;  // per-warp output staging band
     L.off_dy = L.off_stg + (size_t)L.ncw() * L.sb;
     L.off_t = (L.off_dy + (size_t)L.P * L.db + 1023) & ~(size_t)1023;
     const size_t budget = (size_t)env_int("O1D_SMEM_KB", 227) * 1024 - 64;
@@ -1289,6 +1297,7 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.NB = std::max(1, std::min(env_int("O1D_NBUF", 2), std::min(fit, NSmax) / L.P));  // slots per pair
     L.NS = L.P * L.NB;
     L.total = L.off_t + (size_t)L.NS * (L.zb + L.tb) + L.zb;
+    if (L.inslot && L.NB < 2) return lay2(x, geo, es, Hin, wgrad, false);  // the deferred release needs a second slot
     return L;
 }
 
@@ -1330,7 +1339,7 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
 void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool wgrad, int es) {
     const int NB = L.NB, P = L.P;
     const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0);  // exact box bytes
-    const int PQ = P / L.NPROD;  // pairs per producer warp (producer pw serves pairs pw, pw + NPROD, ...)
+    const int PQ = (P + L.NPROD - 1) / L.NPROD;  // pairs per producer warp, at most (producer pw serves pairs pw, pw + NPROD, ...)
     os << "#define P_NB " << PQ * NB << "\n#define PREF " << std::max(1, env_int("O1D_PREF", 2)) << "\n"
        << "  if (warp < " << L.NPROD << ") {\n"
        << "    const int pw = warp;\n"
@@ -1369,12 +1378,12 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
                : "")
        << "    if (early && !p.nowait) pdl_wait();\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
-       << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = 0;\n"
+       << "    for (int qi = 0; qi < " << PQ << "; ++qi) jq[qi] = pw + qi * " << L.NPROD << " < " << P << " ? 0 : -1;\n"
        << (L.BW > 1 ? "    int bq[" + std::to_string(PQ) + "], eq[" + std::to_string(PQ) + "], nq[" + std::to_string(PQ) +
                           "];   // current batch item / next plane / planes, per served pair\n"
                           "    for (int qi = 0; qi < " + std::to_string(PQ) + "; ++qi) { bq[qi] = -1; eq[qi] = 0; nq[qi] = 0; }\n"
                     : "")
-       << "    int issued = 0, fetched = 0, live = " << PQ << ", idle = 0;   // planes issued / scheduler items taken (lane 0)\n"
+       << "    int issued = 0, fetched = 0, live = (" << P + L.NPROD - 1 << " - pw) / " << L.NPROD << ", idle = 0;   // planes issued / scheduler items taken (lane 0)\n"
        << "    while (live > 0) {\n"
        << "      bool any = false;\n"
        << "#pragma unroll 1\n"
@@ -1507,6 +1516,10 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
     "    } else {\n" \
     "      if (lane == 0) trace_ev(p.trace, 2, it, trn);\n" \
     "      mbar_wait(full + s, (it / " << L.NB << ") & 1);\n" \
+    << (L.inslot ? "      if (ps >= 0) {   // previous slot: free once our band store has read it\n" \
+                   "        if (lane == 0) { asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\"); mbar_arrive(empty + ps); }\n" \
+                   "        ps = -1;\n" \
+                   "      }\n" : "") << \
     "      item = s_item[s];\n" \
     "      if (lane == 0) trace_ev(p.trace, 3, item, trn);\n" \
     "      if (item < 0) break;\n" \
@@ -1537,8 +1550,9 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     emit_v2_prologue(os, L, nthreads, false);
     emit_v2_producer(os, x, L, false, es);
     os << "  // -------------------------------------------------------------- consumers\n"
-       << "  unsigned char* const stg = smem + " << L.off_stg << " + cw * " << L.sb << ";   // this warp's output band\n"
+       << (L.inslot ? "" : "  unsigned char* const stg = smem + " + std::to_string(L.off_stg) + " + cw * " + std::to_string(L.sb) + ";   // this warp's output band\n")
        << "  const int row0 = " << 4 * R << " * wg;\n"
+       << (L.inslot ? "  int ps = -1;   // slot whose release waits for this warp's band store\n" : "")
        << (x.order.empty() ? "" : "  int bt = -1; u64 busy = 0; unsigned nbusy = 0;   // adaptive placement accounting\n")
        << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD
@@ -1577,8 +1591,15 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     }
     os << "    }\n"
        << "    if (warm) continue;\n"
-       << "    __syncwarp();\n"
-       << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n";
+       << "    __syncwarp();\n";
+    if (L.inslot) {
+        // both warps of the pair are done reading the slot before either overwrites it
+        if (L.wpg > 1) os << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * L.wpg << ") : \"memory\");\n";
+        os << "    unsigned char* const stg = tile + wg * " << L.sbi << ";   // this warp's output band, in the slot\n"
+           << "    ps = s;\n";
+    } else {
+        os << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n";
+    }
     if (YSTG) {  // O1D_YSTG=1: outputs straight from registers (streaming stores), no staging band
         os << "    if (active) {\n"
            << "      act_t* const yo = reinterpret_cast<act_t*>(p.io) + ((u64)(n * " << x.C << " + c) * " << x.Ho << " + " << R
@@ -1599,7 +1620,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
         return os.str();
     }
     os << ""
-       << (YST ? "" : "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n")
+       << (YST || L.inslot ? "" : "    if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n")
        << "    __syncwarp();\n"
        << "    if (active) {\n"
        << "      act_t* const sto = reinterpret_cast<act_t*>(stg) + (" << R << " * br - row0) * " << x.Wo << " + " << S << " * bc;\n";
