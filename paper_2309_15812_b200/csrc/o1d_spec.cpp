@@ -865,6 +865,108 @@ void emit_stencil_compute_ffma2(std::ostringstream &os, const Geo &g, const std:
     }
 }
 
+// O1D_W8 (v2 stencils, fp32): every lane computes an 8-column block that starts at
+// an even column -- 7*bc for even bc, 7*bc - 1 for odd bc -- and keeps 7 of its 8
+// outputs.  All pixel pairs are then 8-byte aligned and load with one LDS.64 each
+// (with 7-column blocks half the lanes start at an odd column and every pair is
+// two LDS.32); even-dw taps run as 4 FFMA2 per row, odd-dw taps as 3 FFMA2 + 2 FFMA.
+// Off: parity-green but measured 62 vs 44 us forward (166 registers; the 8-byte
+// loads of a half-warp hit 2-way bank conflicts for every pitch with this lane map,
+// and the eighth column adds 14% FMAs)
+#define W8 (env_int("O1D_W8", 0) != 0)
+void emit_stencil_compute_w8(std::ostringstream &os, const Geo &g, const std::vector<int> &ds, const char *ind) {
+    for (int d : ds) {
+        os << ind << "const float m" << d << " = ";
+        for (size_t q = 0; q < g.taps[d].ks.size(); ++q) os << (q ? " + " : "") << "wv[" << g.taps[d].ks[q] << "]";
+        os << ";\n" << ind << "const u64 M" << d << " = f2pack(m" << d << ", m" << d << ");\n";
+    }
+    for (int r = 0; r < R; ++r)
+        os << ind << "u64 A" << r << "_0 = 0ull, A" << r << "_2 = 0ull, A" << r << "_4 = 0ull, A" << r << "_6 = 0ull;\n"
+           << ind << "u64 B" << r << "_1 = 0ull, B" << r << "_3 = 0ull, B" << r << "_5 = 0ull; float B" << r << "_0 = 0.f, B" << r
+           << "_7 = 0.f;\n";
+    int lo_h = 1 << 20, hi_h = -(1 << 20);
+    for (int d : ds) lo_h = std::min(lo_h, g.taps[d].dh), hi_h = std::max(hi_h, g.taps[d].dh);
+    struct Row {
+        int i;
+        std::vector<std::pair<int, int>> pairs;
+        std::set<int> even;   // aligned pairs (e, e + 1) to load
+    };
+    std::vector<Row> rows;
+    for (int i = lo_h; i <= hi_h + R - 1; ++i) {
+        Row rw{i, {}, {}};
+        for (int r = 0; r < R; ++r)
+            for (int d : ds)
+                if (g.taps[d].dh == i - r) rw.pairs.push_back({r, d});
+        if (rw.pairs.empty()) continue;
+        for (auto &p : rw.pairs) {
+            const int dw = g.taps[p.second].dw;
+            for (int s = 0; s < 8; ++s) rw.even.insert((dw + s) & ~1);   // (v & ~1: floor to even, also for v < 0)
+        }
+        rows.push_back(rw);
+    }
+    auto cn = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    auto qname = [&](int i, int e) { return "Q" + cn(i) + "_" + cn(e); };
+    auto scal = [&](int i, int j) {  // pixel j of row i as a float (half of its aligned pair)
+        return std::string("f2") + ((j & 1) ? "hi(" : "lo(") + qname(i, j & ~1) + ")";
+    };
+    const int LA = std::max(0, env_int("O1D_LA", 1));
+    auto loads = [&](const Row &rw) {
+        for (int e : rw.even) {
+            const int off = rw.i * g.pitch + e;   // even: pitch is even and the lane base is even
+            os << ind << "const u64 " << qname(rw.i, e) << " = *reinterpret_cast<const u64*>(tb + " << off << ");\n";
+        }
+    };
+    const int nrows = (int)rows.size();
+    auto chunk_of = [&](int k) { return g_chunks > 1 ? (int)((long)k * g_chunks / nrows) : 0; };
+    Chunker ch{os, ind, nrows, g_chunks};
+    std::map<std::string, long> last_use;
+    long clock = 0;
+    for (int k = 0; k < nrows; ++k) {
+        ch.at(k);
+        const bool first = k == 0 || chunk_of(k - 1) != chunk_of(k);
+        if (first)
+            for (int k2 = k; k2 <= k + LA && k2 < nrows && chunk_of(k2) == chunk_of(k); ++k2) loads(rows[k2]);
+        else if (k + LA < nrows && chunk_of(k + LA) == chunk_of(k))
+            loads(rows[k + LA]);
+        const Row &rw = rows[k];
+        std::vector<std::pair<std::string, std::string>> fm;
+        for (int q = 0; q < 5; ++q)
+            for (auto &p : rw.pairs) {
+                const int r = p.first, d = p.second, dw = g.taps[d].dw;
+                const std::string rs = std::to_string(r);
+                std::ostringstream st;
+                std::string acc;
+                if (((dw % 2) + 2) % 2 == 0) {
+                    if (q == 4) continue;
+                    acc = "A" + rs + "_" + std::to_string(2 * q);
+                    st << acc << " = ffma2(" << qname(rw.i, dw + 2 * q) << ", M" << d << ", " << acc << ");";
+                } else if (q < 3) {
+                    acc = "B" + rs + "_" + std::to_string(2 * q + 1);
+                    st << acc << " = ffma2(" << qname(rw.i, dw + 2 * q + 1) << ", M" << d << ", " << acc << ");";
+                } else {
+                    const int s = q == 3 ? 0 : 7;
+                    acc = "B" + rs + "_" + std::to_string(s);
+                    st << acc << " = fmaf(" << scal(rw.i, dw + s) << ", m" << d << ", " << acc << ");";
+                }
+                fm.push_back({acc, st.str()});
+            }
+        emit_lru(os, ind, fm, last_use, clock);
+    }
+    ch.end();
+    os << ind << "const bool oddb = bc & 1;   // odd lanes keep outputs 1..7 of their block, even lanes 0..6\n";
+    for (int r = 0; r < R; ++r) {
+        const std::string rs = std::to_string(r);
+        os << ind << "{\n"
+           << ind << "  const float o0 = f2lo(A" << rs << "_0) + B" << rs << "_0, o1 = f2hi(A" << rs << "_0) + f2lo(B" << rs << "_1);\n"
+           << ind << "  const float o2 = f2lo(A" << rs << "_2) + f2hi(B" << rs << "_1), o3 = f2hi(A" << rs << "_2) + f2lo(B" << rs << "_3);\n"
+           << ind << "  const float o4 = f2lo(A" << rs << "_4) + f2hi(B" << rs << "_3), o5 = f2hi(A" << rs << "_4) + f2lo(B" << rs << "_5);\n"
+           << ind << "  const float o6 = f2lo(A" << rs << "_6) + f2hi(B" << rs << "_5), o7 = f2hi(A" << rs << "_6) + B" << rs << "_7;\n";
+        for (int c = 0; c < 7; ++c)
+            os << ind << "  a" << rs << "_" << c << " = oddb ? o" << c + 1 << " : o" << c << ";\n";
+        os << ind << "}\n";
+    }
+}
+
 // Warp-specialised stencil kernel (forward / backward_input):
 //   warp 0        producer: schedules planes, stages weights, issues TMA loads
 //                 into a 2-deep ring of tiles (mbarriers full[2] / empty[2])
@@ -1564,11 +1666,14 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     os << "    switch (t) {\n";
     for (int t = 0; t < x.nt; ++t) {
         const Geo &g = geo[t];
+        const bool w8 = W8 && x.ffma2 && x.act == O1D_F32 && L.pitch % 2 == 0;
         os << "    case " << t << ": {\n"
            << "      const act_t* tb = reinterpret_cast<const act_t*>(tile) + (" << R << " * br) * " << L.pitch << " + " << S
-           << " * bc;\n";
+           << " * bc" << (w8 ? " - (bc & 1)" : "") << ";\n";
         const std::vector<int> ds = group_taps(g, 0, 1);
-        if (x.ffma2) {
+        if (w8) {
+            emit_stencil_compute_w8(os, g, ds, "      ");
+        } else if (x.ffma2) {
             emit_stencil_compute_ffma2(os, g, ds, "      ");
         } else {
             for (int r = 0; r < R; ++r)
