@@ -1410,7 +1410,29 @@ std::vector<Geo> geo2(const std::vector<Geo> &geo, const Lay2 &L) {
     return v;
 }
 
-void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool wgrad) {
+// prologue zeroing of the tile area: only what no TMA load ever writes -- the zero-row
+// regions between the slots and each slot's tail past its box -- unless O1D_ZALL=1
+// (every slot byte; ~1 us of stores per CTA at the start of a launch)
+std::string zero_v2(const Lay2 &L, int es, int nthreads) {
+    std::ostringstream os;
+    const size_t box = (size_t)L.hin * L.pitch * es, tail = L.tb - box, stride = L.zb + L.tb;
+    if (env_int("O1D_ZALL", 0) || box % 16 || L.zb % 16) {
+        os << "  for (int i = tid; i < " << (L.total - L.off_t) / 16 << "; i += " << nthreads << ")  // zero rows + slots\n"
+           << "    reinterpret_cast<uint4*>(tiles)[i] = make_uint4(0u, 0u, 0u, 0u);\n";
+        return os.str();
+    }
+    // region s (0..NS): zero rows at s * stride, then (s < NS) the tail of slot s after its box
+    const size_t per = (L.zb + tail) / 16;
+    os << "  for (int i = tid; i < " << (L.NS + 1) * per << "; i += " << nthreads << ") {  // zero rows + slot tails\n"
+       << "    const int s = i / " << per << ", k = i - s * " << per << ";\n"
+       << "    const int off = s * " << stride << " + (k < " << L.zb / 16 << " ? k * 16 : " << L.zb + box << " + (k - " << L.zb / 16
+       << ") * 16);\n"
+       << "    if (s < " << L.NS << " || k < " << L.zb / 16 << ") *reinterpret_cast<uint4*>(tiles + off) = make_uint4(0u, 0u, 0u, 0u);\n"
+       << "  }\n";
+    return os.str();
+}
+
+void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool wgrad, int es) {
     os << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
        << "  u64* const full = reinterpret_cast<u64*>(smem);\n"
        << "  u64* const empty = full + 16;\n"
@@ -1420,8 +1442,7 @@ void emit_v2_prologue(std::ostringstream &os, const Lay2 &L, int nthreads, bool 
        << "  unsigned char* const tiles = smem + " << L.off_t << ";\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
        << "  int trn = 0;\n"
-       << "  for (int i = tid; i < " << (L.total - L.off_t) / 16 << "; i += " << nthreads << ")  // zero rows + slots\n"
-       << "    reinterpret_cast<uint4*>(tiles)[i] = make_uint4(0u, 0u, 0u, 0u);\n"
+       << zero_v2(L, es, nthreads)
        << "  if (tid < " << (16 * 8 + 16 * 4 + 16) / 4 << ") reinterpret_cast<unsigned*>(smem + " << L.off_bal << ")[tid] = 0u;\n"
        << "  if (tid == 0) {\n"
        << "    for (int s = 0; s < " << L.NS << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << L.wpg << "); }\n";
@@ -1649,7 +1670,7 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
     const int es = x.act == O1D_F32 ? 4 : 2;
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_stencil(const __grid_constant__ Params p) {\n";
-    emit_v2_prologue(os, L, nthreads, false);
+    emit_v2_prologue(os, L, nthreads, false, es);
     emit_v2_producer(os, x, L, false, es);
     os << "  // -------------------------------------------------------------- consumers\n"
        << (L.inslot ? "" : "  unsigned char* const stg = smem + " + std::to_string(L.off_stg) + " + cw * " + std::to_string(L.sb) + ";   // this warp's output band\n")
@@ -2048,7 +2069,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "  for (int s = " << NV << "; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);\n"
        << "  return r;\n}\n";
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_wgrad(const __grid_constant__ Params p) {\n";
-    emit_v2_prologue(os, L, nthreads, true);
+    emit_v2_prologue(os, L, nthreads, true, es);
     emit_v2_producer(os, x, L, true, es);
     os << "  float* const scr = reinterpret_cast<float*>(smem + " << L.off_scr << ");\n"
        << "  const act_t* const dys = reinterpret_cast<const act_t*>(smem + " << L.off_dy << " + q * " << L.db << ") + (" << R
