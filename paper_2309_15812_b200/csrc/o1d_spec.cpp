@@ -2619,8 +2619,11 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[3], int nsm, 
                 std::vector<int> work(sp->nt);
                 long mx = 1;
                 for (long c : cost) mx = std::max(mx, c);
+                // per-item cost outside the case (issue units).  Measured flat from 100 to 500 (the
+                // two-SM placement granularity dominates), 0 costs 7% in backward_weight
+                const long ovh = env_int("O1D_COST_OVH", 100);
                 for (int t = 0; t < sp->nt; ++t)
-                    work[t] = (int)std::min<long>(1L << 30, (long)sp->count[t] * (cost[t] + 100) * 1000 / (mx + 100));
+                    work[t] = (int)std::min<long>(1L << 30, (long)sp->count[t] * (cost[t] + ovh) * 1000 / (mx + ovh));
                 xi.home = home_tables(*gpc, work, sp->nt);
                 src[i] = gen();
             }
