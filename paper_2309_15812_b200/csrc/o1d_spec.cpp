@@ -1367,7 +1367,9 @@ Lay2 lay2(const Ctx &x, const std::vector<Geo> &geo, int es, int Hin, bool wgrad
     L.BW = wgrad ? std::max(1, std::min(x.N, env_int("O1D_WB", 1))) : 1;  // (measured: 4 -> 58 us vs 51 us, register pressure)
     L.P = std::max(1, std::min(8, env_int("O1D_P", std::max(1, 8 / x.wpg))));
     while (L.P * L.wpg > 15) --L.P;
-    L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", 2)));   // producer pw serves pairs pw, pw + NPROD, ...
+    // producer pw serves pairs pw, pw + NPROD, ...  Default: one producer per pair up to 4 pairs
+    // (it then sleeps in try_wait; measured +1.8% over two polling producers), else 2
+    L.NPROD = std::max(1, std::min(L.P, env_int("O1D_NPROD", L.P <= 4 ? L.P : 2)));
     for (auto &g : geo) {
         L.pitch = std::max(L.pitch, g.pitch);
         L.zrows = std::max(L.zrows, std::max(-g.minDH, R * x.BR - Hin + g.maxDH) + 1);
@@ -1515,9 +1517,15 @@ void emit_v2_producer(std::ostringstream &os, const Ctx &x, const Lay2 &L, bool 
        << "        const int j = jq[qi];\n"
        << "        if (j < 0) continue;\n"
        << "        const int s = q * " << NB << " + j % " << NB << ";\n"
-       << "        if (j >= " << NB << " && !mbar_test(empty + s, ((j / " << NB << ") & 1) ^ 1)) continue;   // slot still in use\n";
+       << (PQ == 1
+               // one pair per producer: nothing else to serve, so the producer sleeps in
+               // try_wait instead of polling (no issue slots taken from its SM sub-partition)
+               ? "        if (j >= " + std::to_string(NB) + ") mbar_wait(empty + s, ((j / " + std::to_string(NB) + ") & 1) ^ 1);\n"
+               : "        if (j >= " + std::to_string(NB) + " && !mbar_test(empty + s, ((j / " + std::to_string(NB) +
+                     ") & 1) ^ 1)) continue;   // slot still in use\n");
     if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
-        os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
+        os << (PQ == 1 ? "        if (j >= 1) mbar_wait(dyempty + q, ((j - 1) & 1));\n"
+                       : "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n");
     os << "        if (lane == 0) trace_ev(p.trace, 6, q * 65536 + j, trn);   // slot found free\n"
        << "        int item = -1;\n";
     if (L.BW > 1) {
