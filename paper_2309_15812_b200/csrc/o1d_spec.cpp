@@ -2055,7 +2055,9 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
     for (int t = 0; t < x.nt; ++t) maxd = std::max(maxd, (int)geo[t].taps.size());
     int NV = 1;
     while (NV < maxd) NV *= 2;  // reduce-scatter width (<= 32 distinct taps)
-    os << "__constant__ unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
+    // tap -> distinct-tap slot.  In global memory (read through L1): the lanes read 31
+    // different entries at once, which the constant cache would serialise
+    os << (env_int("O1D_K2S_CONST", 0) ? "__constant__" : "__device__ const") << " unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
     for (int t = 0; t < x.nt; ++t) {
         os << (t ? "," : "") << "{";
         for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << geo[t].k2d[k];
@@ -2141,7 +2143,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << "    if (lane < " << NV << ") scr[cw * 32 + lane] = part;\n"
        << "    __syncwarp();\n"
        << "    float* wsp = p.ws + ((u64)(c * " << NBATCH << " + n / " << L.BW << ") * " << L.wpg << " + wg) * " << x.K << ";\n"
-       << "    for (int k = lane; k < " << x.K << "; k += 32) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
+       << "    for (int k = lane; k < " << x.K << "; k += 32) wsp[k] = scr[cw * 32 + " << (env_int("O1D_K2S_CONST", 0) ? "K2S[t][k]" : "__ldg(&K2S[t][k])") << "];\n"
        << "    __syncwarp();\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
        << BAL_ITEM_END
@@ -2270,13 +2272,13 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
         }
     int NV = 1;
     while (NV < maxd) NV *= 2;  // reduce-scatter width (<= 32: K <= 64 and G >= 2, or K <= 32)
-    os << "__constant__ unsigned char K2G[" << x.nt << "][" << x.K << "] = {";
+    os << "__device__ const unsigned char K2G[" << x.nt << "][" << x.K << "] = {";   // global, read via L1 (see gen_wgrad2)
     for (int t = 0; t < x.nt; ++t) {
         os << (t ? "," : "") << "{";
         for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << k2g[t][k];
         os << "}";
     }
-    os << "};\n__constant__ unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
+    os << "};\n__device__ const unsigned char K2S[" << x.nt << "][" << x.K << "] = {";
     for (int t = 0; t < x.nt; ++t) {
         os << (t ? "," : "") << "{";
         for (int k = 0; k < x.K; ++k) os << (k ? "," : "") << k2s[t][k];
@@ -2402,7 +2404,7 @@ std::string gen_wgrad(const Ctx &x, const std::vector<Geo> &geo, const std::vect
        << "    __syncwarp();\n"
        << "    float* wsp = p.ws + ((u64)(c * " << x.N << " + n) * " << x.wpg << " + wg) * " << x.K << ";\n"
        << "    for (int k = lane; k < " << x.K << "; k += 32)\n"
-       << "      if (K2G[t][k] == grp) wsp[k] = scr[cw * 32 + K2S[t][k]];\n"
+       << "      if (__ldg(&K2G[t][k]) == grp) wsp[k] = scr[cw * 32 + __ldg(&K2S[t][k])];\n"
        << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
        << "  }\n"
        << "}\n";
