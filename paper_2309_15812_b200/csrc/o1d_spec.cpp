@@ -1685,7 +1685,10 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
        << "  const int row0 = " << 4 * R << " * wg;\n"
        << (L.inslot ? "  int ps = -1;   // slot whose release waits for this warp's band store\n" : "")
        << (x.order.empty() ? "" : "  int bt = -1; u64 busy = 0; unsigned nbusy = 0;   // adaptive placement accounting\n")
-       << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
+       // O1D_PREWARM bit 1 (bit 2: wgrad): one unguarded pass over the home table's code before
+       // the first tile arrives.  Off: the first plane is then hot, but the cold fetch still
+       // ends at ~7.5 us on the cold tables and the steady tap loop measured 2.56 vs 2.37 us
+       << "  for (int it = " << (g_chunks > 1 || (env_int("O1D_PREWARM", 0) & 1) ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD
        << (x.order.empty() ? "" : "    const long long tb0 = clock64();\n")
        << "    unsigned char* const tile = tiles + " << L.zb << " + s * " << L.zb + L.tb << ";\n"
@@ -2086,7 +2089,7 @@ std::string gen_wgrad2(const Ctx &x, const std::vector<Geo> &geo_in, const std::
        << " * br) * " << L.dyp << " + " << S << " * bc;\n"
        << "  float v[" << NV << "];\n"
        << (x.order.empty() ? "" : "  int bt = -1; u64 busy = 0; unsigned nbusy = 0;   // adaptive placement accounting\n")
-       << "  for (int it = " << (g_chunks > 1 ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
+       << "  for (int it = " << (g_chunks > 1 || (env_int("O1D_PREWARM", 0) & 2) ? -1 : 0) << ";; ++it) {   // it: this pair's item index\n"
        << V2_LOOP_HEAD
        << (x.order.empty() ? "" : "    const long long tb0 = clock64();\n");
     for (int r = 0; r < R; ++r)
