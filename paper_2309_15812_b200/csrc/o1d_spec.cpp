@@ -1696,7 +1696,9 @@ std::string gen_stencil2(const Ctx &x, const std::vector<Geo> &geo_in, const std
     for (int r = 0; r < R; ++r)
         for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
     os << "    switch (t) {\n";
-    for (int t = 0; t < x.nt; ++t) {
+    for (int t0 = 0; t0 < x.nt; ++t0) {
+        // O1D_CASE_REV=1: cases emitted in reverse order (code-layout experiment)
+        const int t = env_int("O1D_CASE_REV", 0) ? x.nt - 1 - t0 : t0;
         const Geo &g = geo[t];
         const bool w8 = W8 && x.ffma2 && x.act == O1D_F32 && L.pitch % 2 == 0;
         os << "    case " << t << ": {\n"
