@@ -105,6 +105,8 @@ if os.environ.get("TRACE_TABLES"):
             print(f"   table {tt}: SMs {len(np.unique(sm[mm]))}, items {mm.sum()}, ends {t[mm].min()/1e3:.1f} .. {t[mm].max()/1e3:.1f}, taps {np.median(dur.get(int(tt), [0]))/1e3:.2f}")
 
 if os.environ.get("TRACE_FIRST"):
+    if os.environ.get("TRACE_FIRST") == "2":  # the same forward twice: is the code still cached?
+        B.forward(plan, x, w)
     torch.cuda._sleep(10_000_000)
     B.forward(plan, x, w)
     tr = plan.debug_trace()
