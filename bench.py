@@ -12,6 +12,10 @@ writes its outputs once: 3 x 154.2 MB fp32) divided by the device time, summed
 over ranks (weak scaling: every rank runs the full configs[1] batch).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f32|bf16] [--impl ours|reference]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU) and fails loudly when fewer than N
+GPUs are visible.
 """
 from __future__ import annotations
 
@@ -48,8 +52,10 @@ def parse():
                     help="s1 = BASELINE configs[1] (default); pp_main / pp_res = the 1D++ block's K=15 main and "
                          "C=384 residual oriented convs (SURVEY NEXT-3); ks = configs[2], the kernel-length sweep "
                          "(N=128, C=384, 14x14, K from --K) with a KxK depthwise conv2d comparator")
-    ap.add_argument("--disc", default="rotation", choices=["rotation", "shear"],
-                    help="tap discretisation: rotation (Def. 1) or shear (Appendix, P:386-440)")
+    ap.add_argument("--disc", default="rotation", choices=["rotation", "shear", "bilinear"],
+                    help="tap discretisation: rotation (Def. 1), shear (Appendix, P:386-440) or bilinear (P:309-311)")
+    ap.add_argument("--fused", type=int, default=None,
+                    help="1: the step's backward is the fused single pass (o1d_backward, NEXT-2); default: the library's")
     ap.add_argument("--model", default=None, choices=["convnext_t_1d", "convnext_b_1d"],
                     help="time the ConvNeXt-1D training step (images/s) instead of the layer step")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch for --model (default 128 T / 64 B)")
@@ -57,6 +63,33 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary bf16 measurement")
     return ap.parse_args()
+
+
+def layer_config(wl, args, world):
+    """`config` of the layer-step line, identical for both arms (--impl ours / reference)."""
+    return {"workload": wl.name, "N_per_gpu": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
+            "angles": (f"D={wl.D} {wl.assign}" if args.angle is None else f"all {args.angle} deg"),
+            "discretization": args.disc, "stride": 1, "layout": "NCHW", "dtype": args.dtype,
+            "parallelism": f"dp{world} (batch-sharded, all-reduce of dW)",
+            "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"}
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (one rank per GPU)."""
+    import socket
+
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < args.gpus:
+        sys.stderr.write(f"bench.py --gpus {args.gpus}: only {n} CUDA device(s) visible on this host\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -146,37 +179,80 @@ def ncu_traffic(pass_name):
         return None
 
 
-def cpu_baseline(wl, dtype_name, target_s=12.0):
-    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _oracle_steps(wl, dtype_name, n, threads, target_s):
+    """Whole 3-pass layer steps of the oracle on n samples until target_s elapsed."""
     import numpy as np
 
     import oracle
     from oracle import taps as T
     from paper_2309_15812_b200 import inputs
 
-    th = max(1, oracle.max_threads())
     angles = T.direction_angles(wl.D, wl.C, wl.assign)
     oh, ow = (np.array(a, np.int32) for a in T.taps_table(wl.K, wl.pad, angles))
-    n = wl.N
     x = inputs.activation((n, wl.C, wl.H, wl.W), 0, dtype_name).astype(np.float64)
     dy = inputs.activation((n, wl.C, wl.H, wl.W), 2, dtype_name).astype(np.float64)
     w = inputs.weights(wl.C, wl.K, 1).astype(np.float64)
     steps = 0
     t0 = time.perf_counter()
     while True:
-        oracle.forward(x, w, oh, ow, 1, th)
-        oracle.backward_input(dy, w, oh, ow, wl.H, wl.W, 1, th)
-        oracle.backward_weight(x, dy, oh, ow, 1, th)
+        oracle.forward(x, w, oh, ow, 1, threads)
+        oracle.backward_input(dy, w, oh, ow, wl.H, wl.W, 1, threads)
+        oracle.backward_weight(x, dy, oh, ow, 1, threads)
         steps += 1
         el = time.perf_counter() - t0
         if el >= target_s or steps >= 100000:
-            break
-    es = 4 if dtype_name == "f32" else 2
+            return steps, el
+
+
+def cpu_baseline(wl, dtype_name, target_s=12.0, full=True):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload
+    (SURVEY 8(d).5): all threads on the workload (the headline `value`), and -- with full --
+    one thread, the fp32-accumulator build, and the K-sweep config at K=31."""
     from dataclasses import replace
+
+    import oracle
+    from paper_2309_15812_b200 import inputs
+
+    es = 4 if dtype_name == "f32" else 2
+    th = max(1, oracle.max_threads())
+    n = min(wl.N, 16)
+    steps, el = _oracle_steps(wl, dtype_name, n, th, target_s)
     bytes_step = sum(algorithmic_bytes(replace(wl, N=n), es).values())
-    return {"value": bytes_step * steps / el / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle",
-            "sample": f"{steps} steps of the 3-pass layer step at N={n} (of {wl.N}), "
-                      f"C={wl.C}, {wl.H}x{wl.W}, K={wl.K}, f64 accumulation, {el:.1f} s"}
+    out = {"value": bytes_step * steps / el / 1e9, "unit": "GB/s", "cores": th, "kind": "oracle",
+           "cpu": cpu_model(),
+           "sample": f"{steps} steps of the 3-pass layer step at N={n} (of {wl.N}), C={wl.C}, {wl.H}x{wl.W}, "
+                     f"K={wl.K}, f64 accumulation, {th} threads, {el:.1f} s"}
+    if full:
+        variants = {}
+        n1 = 1
+        s1, e1 = _oracle_steps(wl, dtype_name, n1, 1, target_s / 4)
+        variants["1_thread"] = {"value": sum(algorithmic_bytes(replace(wl, N=n1), es).values()) * s1 / e1 / 1e9,
+                                "cores": 1, "sample": f"{s1} steps at N={n1}, {e1:.1f} s"}
+        oracle.use_variant("f32acc")
+        try:
+            s2, e2 = _oracle_steps(wl, dtype_name, n, th, target_s / 4)
+        finally:
+            oracle.use_variant("f64")
+        variants["f32_accumulate"] = {"value": bytes_step * s2 / e2 / 1e9, "cores": th,
+                                      "sample": f"{s2} steps at N={n}, fp32 accumulators, {e2:.1f} s"}
+        ks = inputs.ksweep(31)
+        nk = 8
+        s3, e3 = _oracle_steps(ks, dtype_name, nk, th, target_s / 4)
+        variants["ksweep_k31"] = {"value": sum(algorithmic_bytes(replace(ks, N=nk), es).values()) * s3 / e3 / 1e9,
+                                  "cores": th, "sample": f"{s3} steps of configs[2] K=31 at N={nk}, {e3:.1f} s"}
+        out["variants"] = variants
+    return out
 
 
 def run_reference(args):
@@ -185,17 +261,27 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_2309_15812_b200 import inputs
-    wl = inputs.WORKLOADS[args.workload]
-    cb = cpu_baseline(wl, args.dtype, target_s=max(2.0, 60.0 / max(1, args.steps + args.warmup)))
+    wl = inputs.ksweep(args.K or 31) if args.workload == "ks" else inputs.WORKLOADS[args.workload]
+    cb = cpu_baseline(wl, args.dtype, target_s=max(2.0, 60.0 / max(1, args.steps + args.warmup)), full=False)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64)",
-            "config": {"workload": wl.name, "N": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
-                       "angles": f"D={wl.D} {wl.assign}", "stride": 1},
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64 U[-1,1))",
+            "config": layer_config(wl, args, args.gpus),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ffma_peak():
+    """Measured FP32 FMA peak (TFLOP/s) of this pool's B200 (profiles/r2/ffma_peak.json,
+    tools/ffma2_bench.cu), else the nominal 148 SMs x 128 FMA/clk x 1.965 GHz."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "ffma_peak.json")) as f:
+            d = json.load(f)
+        return float(d["ffma_tflops"]), "measured (profiles/r2/ffma_peak.json, tools/ffma2_bench.cu)"
+    except Exception:
+        return 2 * 148 * 128 * 1.965e9 / 1e12, "nominal (148 SMs x 128 FMA/clk x 1.965 GHz)"
 
 
 def run_model(args):
@@ -284,17 +370,20 @@ def run_ours(args):
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.dtype]
     es = 4 if args.dtype == "f32" else 2
     wl = inputs.ksweep(args.K or 31) if args.workload == "ks" else inputs.WORKLOADS[args.workload]
+    from dataclasses import replace
     if args.dirs is not None:
-        from dataclasses import replace
         wl = replace(wl, D=args.dirs)
     if args.K is not None:
-        from dataclasses import replace
         wl = replace(wl, K=args.K)
     angles = B.direction_angles(wl.D, wl.C, wl.assign)
     if args.angle is not None:
         angles = np.full(wl.C, float(args.angle))
+    if args.fused is not None:
+        os.environ["O1D_FUSED"] = str(args.fused)
     plan = B.Plan(wl.N, wl.C, wl.H, wl.W, wl.K, angles, dtype=tdt, flags=args.flags, device=dev,
                   discretization=args.disc)
+    plan_ms, cache_hit = plan.stats()
+    fused_step = "step=fused" in plan.describe()
     # two rotating buffer sets so every pass streams from HBM (each set 4 x 77 MB > L2)
     sets = []
     for s in range(2):
@@ -305,32 +394,29 @@ def run_ours(args):
     dW = torch.empty_like(w)
     ws = B.workspace(plan)
     stream = torch.cuda.current_stream()
+    NPASS = ("forward", "backward_input", "backward_weight", "backward_fused")
 
     def step(i, ev=None):
         b = sets[i & 1]
-        if ev is None and os.environ.get("BENCH_STEP_API", "1") == "1":
+        if ev is None:
             B.step(plan, b["x"], w, b["dy"], b["y"], b["dx"], dW, ws)  # o1d_step: passes overlap
             if world > 1:
-                dp.allreduce_weight_grad(dW)
+                dp.allreduce_weight_grad(dW)  # row a8: NCCL sum of the weight gradient over NVLink
             return
-        if ev is not None:
-            ev[0].record(stream)
+        ev[0].record(stream)
         B.forward(plan, b["x"], w, b["y"])
-        if ev is not None:
-            ev[1].record(stream)
+        ev[1].record(stream)
         B.backward_input(plan, b["dy"], w, b["dx"])
-        if ev is not None:
-            ev[2].record(stream)
+        ev[2].record(stream)
         B.backward_weight(plan, b["x"], b["dy"], dW, ws)
-        if ev is not None:
-            ev[3].record(stream)
-        if world > 1:
-            dp.allreduce_weight_grad(dW)  # row a8: NCCL sum of the weight gradient over NVLink
+        ev[3].record(stream)
+        B.backward(plan, b["x"], b["dy"], w, b["dx"], dW, ws)
+        ev[4].record(stream)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -345,30 +431,37 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # per-pass times (the roofline of the dominant kernel): the same steps as three separate
-    # calls with CUDA events between them, timed in a second loop
+    # per-pass times (the roofline of the dominant kernel): the same passes as separate calls
+    # with CUDA events between them, timed in a second loop (each kernel in isolation)
     for i in range(args.steps):
         step(i, evs[i])
     torch.cuda.synchronize()
     ck = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
-    per_pass = {p: 0.0 for p in PASSES}
+    per_pass = {p: 0.0 for p in NPASS}
     for e in evs:
-        for j, p in enumerate(PASSES):
+        for j, p in enumerate(NPASS):
             per_pass[p] += e[j].elapsed_time(e[j + 1])
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     ab = algorithmic_bytes(wl, es)
-    bytes_step = sum(ab.values())
+    # fused backward: reads x and dy once, writes dx (+ w read, dW written): 3 planes per (n, c)
+    plane_b = wl.N * wl.C * wl.H * wl.W * es
+    ab["backward_fused"] = 3 * plane_b + 2 * wl.C * wl.K * 4
+    bytes_step = sum(ab[p] for p in PASSES)  # the step's algorithmic bytes (three-pass accounting)
     value = bytes_step * args.steps * world / (max_ms * 1e-3) / 1e9
     ms_step = max_ms / args.steps
     peak, peak_src = measured_peaks()
-    dom = max(PASSES, key=lambda p: per_pass[p])
+    timed = ("forward", "backward_fused") if fused_step else PASSES
+    dom = max(timed, key=lambda p: per_pass[p])
     dom_ms = per_pass[dom] / args.steps
     achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
-    launches = sum(plan.launches_per_call(j) for j in range(3)) * args.steps
+    launches = (plan.launches_per_call(0) + (plan.launches_per_call(3) if fused_step else
+                                            plan.launches_per_call(1) + plan.launches_per_call(2))) * args.steps
+    fpk, fpk_src = ffma_peak()
+    fmas_pass = algorithmic_fmas(wl)
 
     # end to end through the C ABI with pinned HOST buffers (H2D + 3 passes + D2H per step)
     e2e = None
@@ -401,18 +494,26 @@ def run_ours(args):
 
     extra = {}
     if rank == 0:
-        extra["per_pass_ms"] = {p: per_pass[p] / args.steps for p in PASSES}
-        extra["per_pass_gbs"] = {p: ab[p] / (per_pass[p] / args.steps * 1e-3) / 1e9 for p in PASSES}
-        extra["per_pass_frac_of_hbm"] = {p: extra["per_pass_gbs"][p] / peak for p in PASSES}
-        extra["fp32_tflops_dense"] = 3 * 2 * algorithmic_fmas(wl) / (ms_step * 1e-3) / 1e12
+        extra["per_pass_ms"] = {p: per_pass[p] / args.steps for p in NPASS}
+        extra["per_pass_gbs"] = {p: ab[p] / (per_pass[p] / args.steps * 1e-3) / 1e9 for p in NPASS}
+        extra["per_pass_frac_of_hbm"] = {p: extra["per_pass_gbs"][p] / peak for p in NPASS}
+        extra["per_pass_frac_of_ffma"] = {p: (2 if p == "backward_fused" else 1) * 2 * fmas_pass /
+                                          (per_pass[p] / args.steps * 1e-3) / 1e12 / fpk for p in NPASS}
+        extra["ffma_peak_tflops"] = {"value": fpk, "source": fpk_src}
+        extra["algorithmic_bytes"] = ab
+        extra["fp32_tflops_dense"] = 3 * 2 * fmas_pass / (ms_step * 1e-3) / 1e12
         extra["imgs_per_s_layer_step"] = wl.N * world / (ms_step * 1e-3)
         extra["plan"] = plan.describe()
+        extra["plan_create_ms"] = plan_ms
+        extra["plan_jit_cache_hit"] = cache_hit
+        extra["step_backward"] = "fused single pass (o1d_backward)" if fused_step else "backward_input + backward_weight"
         if args.workload == "ks":
             # configs[2] "vs equivalent kxk depthwise (linear-cost check)": torch conv2d (cuDNN),
             # groups=C, K x K, same activations, forward + both gradients -- a library comparator
             xk = sets[0]["x"].detach().clone().requires_grad_(True)
             wk = torch.randn(wl.C, 1, wl.K, wl.K, device=dev, dtype=tdt, requires_grad=True)
             gk = sets[0]["dy"]
+
             def kxk():
                 yk = torch.nn.functional.conv2d(xk, wk, padding=wl.K // 2, groups=wl.C)
                 yk.backward(gk)
@@ -429,22 +530,23 @@ def run_ours(args):
             extra["comparator"] = {"what": f"torch conv2d depthwise {wl.K}x{wl.K} fwd+bwd (cuDNN), same shape",
                                    "ms_per_step": t0k.elapsed_time(t1k) / nk, "ours_ms_per_step": ms_step,
                                    "ours_speedup": (t0k.elapsed_time(t1k) / nk) / ms_step}
+    bound_alu = args.dtype != "f32"
+    roof = {"kernel": dom, "unit": "GB/s", "algorithmic_bytes_per_launch": ab[dom], "peak_source": peak_src}
+    if bound_alu:
+        # 16-bit activations: arithmetic intensity 15.5 flop/B > the FFMA/HBM ridge -> FFMA bound
+        fl = (2 if dom == "backward_fused" else 1) * 2 * fmas_pass / (dom_ms * 1e-3) / 1e12
+        roof.update({"bound": "alu", "achieved": fl, "peak": fpk, "unit": "TFLOP/s", "frac": fl / fpk,
+                     "peak_source": fpk_src, "hbm_gbs": achieved, "hbm_frac": achieved / peak, "traffic": None})
+    else:
+        roof.update({"bound": "hbm", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+                     "traffic": ncu_traffic(dom) if args.angle is None and args.disc == "rotation" else None,
+                     "traffic_source": "profiles/traffic.json (ncu --set full, fp32 S1)"})
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded SplitMix64 U[-1,1))",
-        "config": {"workload": wl.name, "N_per_gpu": wl.N, "C": wl.C, "H": wl.H, "W": wl.W, "K": wl.K,
-                   "angles": (f"D={wl.D} {wl.assign}" if args.angle is None else f"all {args.angle} deg")
-                   + ("" if args.disc == "rotation" else f", {args.disc} taps"),
-                   "stride": 1, "layout": "NCHW",
-                   "parallelism": f"dp{world} (batch-sharded, NCCL all-reduce of dW)",
-                   "l2": "inputs > L2: 2 rotating buffer sets of 4 x 77 MB"},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak,
-                     "traffic": ncu_traffic(dom) if args.dtype == "f32" and args.angle is None else None,
-                     "traffic_source": "profiles/traffic.json (ncu --set full, fp32 S1)",
-                     "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": ab[dom]},
+        "config": layer_config(wl, args, world),
+        "roofline": roof,
         "gpu_launches": launches, "clocks": ck, "e2e": e2e,
     }
     line.update(extra)
@@ -453,27 +555,29 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(wl, args.dtype)
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"error": repr(ex)}
+
+    def sub(extra_args, timeout):
+        out = subprocess.run([sys.executable, os.path.abspath(__file__)] + extra_args, capture_output=True, text=True,
+                             timeout=timeout, env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
+        return json.loads(out.stdout.strip().splitlines()[-1])
     if rank == 0 and not args.no_extra and args.dtype == "f32":
+        common = ["--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu", "--no-extra",
+                  "--flags", str(args.flags)]
+        for key, ex in (("bf16", ["--dtype", "bf16"]), ("bilinear", ["--disc", "bilinear"])):
+            try:
+                b = sub(ex + common, 600)
+                line[key] = {k: b[k] for k in ("value", "ms_per_step", "roofline", "per_pass_ms", "per_pass_gbs",
+                                               "per_pass_frac_of_hbm", "per_pass_frac_of_ffma", "plan_create_ms")}
+            except Exception as ex_:  # pragma: no cover
+                line[key] = {"error": repr(ex_)}
         try:
-            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--dtype", "bf16", "--steps",
-                                  str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu",
-                                  "--no-extra", "--flags", str(args.flags)],
-                                 capture_output=True, text=True, timeout=600,
-                                 env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
-            b = json.loads(out.stdout.strip().splitlines()[-1])
-            line["bf16"] = {k: b[k] for k in ("value", "ms_per_step", "roofline", "per_pass_gbs",
-                                              "per_pass_frac_of_hbm")}
-        except Exception as ex:  # pragma: no cover
-            line["bf16"] = {"error": repr(ex)}
-    if rank == 0 and not args.no_extra and args.dtype == "f32":
-        try:
-            out = subprocess.run([sys.executable, os.path.abspath(__file__), "--model", "convnext_t_1d", "--steps", "10",
-                                  "--warmup", "3"], capture_output=True, text=True, timeout=900,
-                                 env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
-            m = json.loads(out.stdout.strip().splitlines()[-1])
-            line["convnext_t_1d_train"] = {k: m[k] for k in ("value", "unit", "ms_per_step", "config")}
-        except Exception as ex:  # pragma: no cover
-            line["convnext_t_1d_train"] = {"error": repr(ex)}
+            m = sub(["--model", "convnext_t_1d", "--steps", "10", "--warmup", "3"], 900)
+            line["convnext_t_1d_train"] = {k: m[k] for k in ("value", "unit", "ms_per_step", "config") if k in m}
+            for k in ("oriented_share", "comparator"):
+                if k in m:
+                    line["convnext_t_1d_train"][k] = m[k]
+        except Exception as ex_:  # pragma: no cover
+            line["convnext_t_1d_train"] = {"error": repr(ex_)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -483,6 +587,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.model:

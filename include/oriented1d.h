@@ -68,13 +68,15 @@ typedef enum { O1D_NCHW = 0 } o1d_layout;
 typedef enum { O1D_ASSIGN_CONTIGUOUS = 0, O1D_ASSIGN_CYCLED = 1 } o1d_assign;
 
 /* Problem descriptor (Def. 1): N batch, C channels, H x W input, K taps, stride
- * `stride` on both axes, padding `pad` (pass -1 for the paper's default
- * floor(K/2); otherwise 0 <= pad < K), activation dtype and layout.
- * `flags` selects implementation options (O1D_FLAG_*), 0 = library default.  */
+ * `stride` on both axes, padding `pad` (a real number, Def. 1 / Eq. coordinate1d
+ * P:346-351 write pad_w without restricting it to integers; pass any negative
+ * value for the paper's default floor(K/2); otherwise 0 <= pad <= K-1),
+ * activation dtype and layout.  `flags` selects the discretisation and
+ * implementation options (O1D_FLAG_*), 0 = library default.  */
 typedef struct {
     int32_t N, C, H, W, K;
     int32_t stride;
-    int32_t pad;
+    double pad;
     int32_t dtype;   /* o1d_dtype  */
     int32_t layout;  /* o1d_layout */
     int32_t flags;
@@ -88,6 +90,12 @@ typedef struct {
  * default = rotation (Def. 1); O1D_FLAG_SHEAR = the shear parameterisation of the
  * Appendix "Rotation vs Shearing", see o1d_make_taps_ex. */
 #define O1D_FLAG_SHEAR         0x4
+/* O1D_FLAG_BILINEAR = the bilinear-interpolation discretisation of P:309-311 (Sec.
+ * "Discretization and Interpolation", Table "bilinear" P:322-334): each tap samples x at
+ * the REAL coordinate of Eq. coordinate2d, (str*p - (k-pad) sin t, str*q + (k-pad) cos t),
+ * interpolated from its four integer neighbours (zero outside the image).  See
+ * o1d_make_bilinear.  Mutually exclusive with O1D_FLAG_SHEAR. */
+#define O1D_FLAG_BILINEAR      0x8
 
 typedef struct o1d_plan o1d_plan;
 
@@ -98,8 +106,11 @@ typedef struct o1d_plan o1d_plan;
  * the product is evaluated exactly, elsewhere it is irrational and its floor is
  * taken from f64 trig, re-evaluated in binary128 when within 1e-9 of an integer.
  * angles_deg: host [C] (degrees, any finite real).  oh, ow: host [C][K] outputs.
- * pad: -1 => floor(K/2).  Pure host function, no CUDA context needed. */
-O1D_API o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double *angles_deg,
+ * pad: any negative value => floor(K/2); otherwise a finite real |pad| <= 4096 (k - pad
+ * is then a binary double, so the same exactness argument holds).  Pure host
+ * function, no CUDA context needed.  Errors: INVALID_ARG (NULL, non-finite angle or
+ * pad), INVALID_CONFIG (K < 1, |pad| > 4096), INVALID_SHAPE (C < 1). */
+O1D_API o1d_status o1d_make_taps(int32_t K, double pad, int32_t C, const double *angles_deg,
                          int16_t *oh, int16_t *ow);
 
 /* Tap-offset table for discretisation `mode`: O1D_TAPS_ROTATION (= o1d_make_taps) or
@@ -112,8 +123,20 @@ O1D_API o1d_status o1d_make_taps(int32_t K, int32_t pad, int32_t C, const double
  * Same arguments, ownership and errors as o1d_make_taps; INVALID_ARG for a bad mode. */
 #define O1D_TAPS_ROTATION 0
 #define O1D_TAPS_SHEAR    1
-O1D_API o1d_status o1d_make_taps_ex(int32_t K, int32_t pad, int32_t C, const double *angles_deg, int32_t mode,
+#define O1D_TAPS_BILINEAR 2   /* the base (floor) corner of each bilinear tap = the rotation taps */
+O1D_API o1d_status o1d_make_taps_ex(int32_t K, double pad, int32_t C, const double *angles_deg, int32_t mode,
                                     int16_t *oh, int16_t *ow);
+
+/* Bilinear discretisation (O1D_FLAG_BILINEAR): tap k of channel c samples x at
+ * the real offset (u, v) = (-(k-pad) sin t, (k-pad) cos t) from the output's anchor.  With
+ * h0 = floor(u), w0 = floor(v) (exact floors, = o1d_make_taps) and the fractional parts
+ * a = u - h0, b = v - w0 in [0, 1) (exact 0 / 1/2 at the Niven angles, else f64 trig), the
+ * tap reads
+ *     (1-a)(1-b) x[h0][w0] + (1-a) b x[h0][w0+1] + a (1-b) x[h0+1][w0] + a b x[h0+1][w0+1]
+ * (zero outside the image; reading R14).  h0, w0: host int16 [C][K]; fa, fb: host f64 [C][K].
+ * Arguments and errors as o1d_make_taps. */
+O1D_API o1d_status o1d_make_bilinear(int32_t K, double pad, int32_t C, const double *angles_deg, int16_t *h0,
+                                     int16_t *w0, double *fa, double *fb);
 
 /* Per-channel angles from D directions: angle_i = i*180/D deg,
  * channels split into D equal groups; group(c) = floor(c*D/C) for
@@ -125,17 +148,26 @@ O1D_API o1d_status o1d_direction_angles(int32_t D, int32_t C, int32_t assign, do
 
 /* Create an immutable plan for descriptor `d` and per-channel angles
  * angles_deg (host [C], degrees).  Computes the tap tables (as
- * o1d_make_taps), de-duplicates equal tables, derives halo extents, selects
- * (and, unless O1D_FLAG_FORCE_GENERIC, JIT-specialises) the kernels and uploads
- * the tables to the current CUDA device.  *out receives the plan (NULL on
- * error).  Must be called with the target device current. */
+ * o1d_make_taps / o1d_make_bilinear), de-duplicates equal tables, derives halo
+ * extents, selects (and, unless O1D_FLAG_FORCE_GENERIC, JIT-specialises) the kernels
+ * and uploads the tables to the current CUDA device.  Specialised modules are cached
+ * per process and device by their generated source, which does not depend on N: plans
+ * that differ only in the batch size (or are re-created) share the compiled code.
+ * *out receives the plan (NULL on error).  Must be called with the target device
+ * current. */
 O1D_API o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan **out);
 
 /* Output size: P = (H-1)/stride + 1, Q = (W-1)/stride + 1. */
 O1D_API o1d_status o1d_plan_out_shape(const o1d_plan *plan, int32_t *P, int32_t *Q);
 
-/* Copy the plan's tap table to host oh, ow [C][K]. */
+/* Copy the plan's tap table to host oh, ow [C][K] (bilinear plans: the base corners). */
 O1D_API o1d_status o1d_plan_get_taps(const o1d_plan *plan, int16_t *oh, int16_t *ow);
+
+/* Plan-creation cost: host milliseconds spent in o1d_plan_create (tap tables, source
+ * generation, NVRTC compile or module-cache hit, module load) and whether the
+ * specialised modules came from the process-wide cache (1) or were compiled (0; -1 when
+ * the plan has no specialised kernels). */
+O1D_API o1d_status o1d_plan_stats(const o1d_plan *plan, double *create_ms, int32_t *jit_cache_hit);
 
 /* Short NUL-terminated description of the kernels the plan selected
  * (family, tile shape, number of specialised tap tables). */
@@ -161,6 +193,16 @@ O1D_API o1d_status o1d_backward_input(const o1d_plan *plan, const void *dy, cons
  * Deterministic: partial sums are reduced in a fixed order. */
 O1D_API o1d_status o1d_backward_weight(const o1d_plan *plan, const void *x, const void *dy, float *dW,
                                void *ws, size_t ws_bytes, void *stream);
+
+/* Fused backward: backward_input and backward_weight in ONE pass over x
+ * and dy -- every (n, c) plane of x and dy is read from HBM once and both dx and the dW
+ * partials are produced from the same shared-memory tiles (plus the fixed-order dW
+ * finalize launch).  Same results as o1d_backward_input + o1d_backward_weight (dx
+ * bitwise; dW bitwise, the same partial sums in the same order).  Buffers as for those
+ * two calls; ws >= o1d_workspace_bytes(plan).  Plans without the fused kernel run the
+ * two passes. */
+O1D_API o1d_status o1d_backward(const o1d_plan *plan, const void *x, const void *dy, const float *w, void *dx,
+                                float *dW, void *ws, size_t ws_bytes, void *stream);
 
 /* One training step of the layer through HOST buffers (the end-to-end path):
  * copies x, w, dy host->device, runs forward, backward_input and
@@ -189,9 +231,13 @@ O1D_API o1d_status o1d_step_host(const o1d_plan *plan, const void *x_h, const fl
 O1D_API o1d_status o1d_step(const o1d_plan *plan, const void *x, const float *w, const void *dy, void *y, void *dx,
                             float *dW, void *ws, size_t ws_bytes, void *stream);
 
-/* Number of kernel launches one call of each pass issues (for launch accounting). */
-O1D_API int32_t o1d_launches_per_call(const o1d_plan *plan, int32_t pass /* 0 fwd, 1 bwd_in, 2 bwd_w */);
+/* Number of kernel launches one call of each pass issues (for launch accounting);
+ * pass 3 = o1d_backward. */
+O1D_API int32_t o1d_launches_per_call(const o1d_plan *plan, int32_t pass /* 0 fwd, 1 bwd_in, 2 bwd_w, 3 fused bwd */);
 
+/* Destroy a plan: makes the plan's device current, waits for the device's outstanding
+ * work (a launch may still reference the plan's tables and scheduler counters), releases
+ * its resources and restores the caller's current device.  NULL is a no-op. */
 O1D_API void o1d_plan_destroy(o1d_plan *plan);
 
 /* Diagnostics: the CUDA C++ source the plan's specialised kernels would be

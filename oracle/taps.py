@@ -9,6 +9,8 @@ What it computes:
         oh_k = floor( -(k - pad) * sin(theta) ),   ow_k = floor( (k - pad) * cos(theta) )
     the floor of the EXACT real value (reading R3).
   * Direction groups: D angles i*180/D, channels split into D equal groups.
+  * Bilinear discretisation: base corners + fractional parts of the real
+    offsets (bilinear_exact / bilinear_table).
 
 Exactness: the angle is a binary double, i.e. a rational number of degrees.  By
 Niven's theorem sin(t deg) for rational t is rational only when it is 0, +-1/2 or
@@ -38,18 +40,29 @@ def _reduce_deg(theta_deg: float) -> Fraction:
     return Fraction(theta_deg) % 360
 
 
-def _exact_floor_times(m: int, t: Fraction, fn: str) -> int:
-    """floor(m * fn(t degrees)) exactly, fn in {"sin", "cos"}."""
-    if m == 0:
-        return 0
+def _exact_value_times(m: Fraction, t: Fraction, fn: str):
+    """m * fn(t degrees): an exact Fraction at the Niven angles, else an 80-digit mpf
+    (irrational for m != 0)."""
     table = _SIN_RATIONAL if fn == "sin" else _COS_RATIONAL
+    if m == 0:
+        return Fraction(0)
     if t.denominator == 1 and int(t) in table:
-        v = m * table[int(t)]
-        return v.numerator // v.denominator  # Fraction floor
+        return m * table[int(t)]
     with mpmath.workdps(_DPS):
         tt = mpmath.mpf(t.numerator) / t.denominator
         rad = tt * mpmath.pi / 180
-        v = m * (mpmath.sin(rad) if fn == "sin" else mpmath.cos(rad))
+        mm = mpmath.mpf(m.numerator) / m.denominator
+        return mm * (mpmath.sin(rad) if fn == "sin" else mpmath.cos(rad))
+
+
+def _exact_floor_times(m, t: Fraction, fn: str) -> int:
+    """floor(m * fn(t degrees)) exactly, fn in {"sin", "cos"}; m = k - pad is rational
+    (pad may be any binary double, Eq. coordinate1d)."""
+    m = Fraction(m)
+    v = _exact_value_times(m, t, fn)
+    if isinstance(v, Fraction):
+        return v.numerator // v.denominator  # Fraction floor
+    with mpmath.workdps(_DPS):
         f = int(mpmath.floor(v))
         dist = min(v - f, f + 1 - v)
         # irrational (Niven) => not an integer; must be resolvable at this precision
@@ -57,16 +70,57 @@ def _exact_floor_times(m: int, t: Fraction, fn: str) -> int:
     return f
 
 
-def taps_exact(K: int, pad: int, theta_deg: float):
-    """Exact tap table for one angle: list of (oh_k, ow_k), k = 0..K-1."""
+def taps_exact(K: int, pad, theta_deg: float):
+    """Exact tap table for one angle: list of (oh_k, ow_k), k = 0..K-1.
+    pad: an int or any float (taken as its exact binary value)."""
     t = _reduce_deg(theta_deg)
     out = []
     for k in range(K):
-        m = k - pad
+        m = k - Fraction(pad)
         oh = _exact_floor_times(-m, t, "sin")   # floor(-(k-pad) sin θ)
         ow = _exact_floor_times(m, t, "cos")    # floor( (k-pad) cos θ)
         out.append((oh, ow))
     return out
+
+
+def bilinear_exact(K: int, pad, theta_deg: float):
+    """Bilinear discretisation (Sec. "Discretization and Interpolation"): tap k
+    samples x at the REAL offset of Eq. coordinate2d restricted to the 1D
+    kernel (r = 0, s = k, pad_w = pad):  (u, v) = (-(k-pad) sin θ, (k-pad) cos θ).
+    Returns per tap (h0, w0, a, b): the integer base corner h0 = floor(u), w0 = floor(v)
+    (exact, = taps_exact) and the fractional parts a = u - h0, b = v - w0 in [0, 1)
+    (exact at the Niven angles, else evaluated at 80 digits and rounded to f64).  The
+    interpolated sample is (1-a)(1-b) x[h0][w0] + (1-a) b x[h0][w0+1] + a (1-b) x[h0+1][w0]
+    + a b x[h0+1][w0+1] (reading R14)."""
+    t = _reduce_deg(theta_deg)
+    out = []
+    for k in range(K):
+        m = k - Fraction(pad)
+        u = _exact_value_times(-m, t, "sin")
+        v = _exact_value_times(m, t, "cos")
+        h0 = _exact_floor_times(-m, t, "sin")
+        w0 = _exact_floor_times(m, t, "cos")
+        with mpmath.workdps(_DPS):
+            a = float(u - h0) if isinstance(u, Fraction) else float(u - h0)
+            b = float(v - w0) if isinstance(v, Fraction) else float(v - w0)
+        out.append((h0, w0, a, b))
+    return out
+
+
+def bilinear_table(K: int, pad, angles_deg):
+    """Per-channel bilinear tables: (h0[C][K], w0[C][K], a[C][K], b[C][K]) nested lists."""
+    cache = {}
+    h0, w0, fa, fb = [], [], [], []
+    for ang in angles_deg:
+        key = float(ang)
+        if key not in cache:
+            cache[key] = bilinear_exact(K, pad, key)
+        rows = cache[key]
+        h0.append([r[0] for r in rows])
+        w0.append([r[1] for r in rows])
+        fa.append([r[2] for r in rows])
+        fb.append([r[3] for r in rows])
+    return h0, w0, fa, fb
 
 
 # Shear parameterisation (Appendix "Rotation vs Shearing", P:386-440).  The filter
@@ -125,7 +179,7 @@ def taps_exact_shear(K: int, pad: int, theta_deg: float):
             for k in range(K)]
 
 
-def taps_table(K: int, pad: int, angles_deg, mode: str = "rotation"):
+def taps_table(K: int, pad, angles_deg, mode: str = "rotation"):
     """Per-channel tables: (oh[C][K], ow[C][K]) as nested lists of int.  mode:
     "rotation" (Def. 1, the paper's default) or "shear" (Appendix)."""
     if mode not in ("rotation", "shear"):

@@ -25,14 +25,16 @@ DTYPES = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
 FLAG_FORCE_GENERIC = 0x1
 FLAG_NO_TMA = 0x2
 FLAG_SHEAR = 0x4
-TAPS = {"rotation": 0, "shear": 1}
+FLAG_BILINEAR = 0x8
+TAPS = {"rotation": 0, "shear": 1, "bilinear": 2}
 ASSIGN = {"contiguous": 0, "cycled": 1}
 
 EXPORTS = ["o1d_make_taps", "o1d_direction_angles", "o1d_plan_create", "o1d_plan_out_shape",
            "o1d_plan_get_taps", "o1d_plan_describe", "o1d_workspace_bytes", "o1d_forward",
            "o1d_backward_input", "o1d_backward_weight", "o1d_step_host_workspace_bytes", "o1d_step_host",
            "o1d_launches_per_call", "o1d_plan_destroy", "o1d_last_error", "o1d_version", "o1d_spec_source",
-           "o1d_debug_trace", "o1d_make_taps_ex", "o1d_step"]
+           "o1d_debug_trace", "o1d_make_taps_ex", "o1d_step", "o1d_make_bilinear", "o1d_plan_stats",
+           "o1d_backward"]
 
 
 class O1DError(RuntimeError):
@@ -42,7 +44,8 @@ class O1DError(RuntimeError):
 
 
 class _Desc(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int32) for n in ("N", "C", "H", "W", "K", "stride", "pad", "dtype", "layout", "flags")]
+    _fields_ = ([(n, ctypes.c_int32) for n in ("N", "C", "H", "W", "K", "stride")] + [("pad", ctypes.c_double)]
+                + [(n, ctypes.c_int32) for n in ("dtype", "layout", "flags")])
 
 
 _lib = None
@@ -60,7 +63,7 @@ def lib():
             L = ctypes.CDLL(LIB_PATH)
             st, vp, i32, i16p, f64p = ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
             sig = {
-                "o1d_make_taps": (st, [i32, i32, i32, f64p, i16p, i16p]),
+                "o1d_make_taps": (st, [i32, ctypes.c_double, i32, f64p, i16p, i16p]),
                 "o1d_direction_angles": (st, [i32, i32, i32, ctypes.c_double, f64p]),
                 "o1d_plan_create": (st, [ctypes.POINTER(_Desc), f64p, ctypes.POINTER(vp)]),
                 "o1d_plan_out_shape": (st, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
@@ -77,8 +80,11 @@ def lib():
                 "o1d_last_error": (ctypes.c_char_p, []),
                 "o1d_version": (ctypes.c_char_p, []),
                 "o1d_debug_trace": (ctypes.c_size_t, [vp, vp, ctypes.c_size_t]),
-                "o1d_make_taps_ex": (st, [i32, i32, i32, f64p, i32, i16p, i16p]),
+                "o1d_make_taps_ex": (st, [i32, ctypes.c_double, i32, f64p, i32, i16p, i16p]),
+                "o1d_make_bilinear": (st, [i32, ctypes.c_double, i32, f64p, i16p, i16p, f64p, f64p]),
+                "o1d_plan_stats": (st, [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]),
                 "o1d_step": (st, [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+                "o1d_backward": (st, [vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
                 "o1d_spec_source": (st, [ctypes.POINTER(_Desc), f64p, i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
             }
             for name, (res, args) in sig.items():
@@ -102,17 +108,29 @@ def version() -> str:
     return lib().o1d_version().decode()
 
 
-def make_taps(K: int, angles_deg, pad: int = -1, discretization: str = "rotation"):
+def make_taps(K: int, angles_deg, pad: float = -1, discretization: str = "rotation"):
     """Tap tables (oh, ow) int16 [C][K] from the library's host tap generator;
-    discretization "rotation" (Def. 1) or "shear" (Appendix, P:386-440)."""
+    discretization "rotation" (Def. 1), "shear" (Appendix, P:386-440) or "bilinear"
+    (the base corners).  pad: a real number, negative = floor(K/2)."""
     a = np.ascontiguousarray(angles_deg, dtype=np.float64)
     C = a.shape[0]
     oh = np.empty((C, K), np.int16)
     ow = np.empty((C, K), np.int16)
     if discretization not in TAPS:
-        raise ValueError("discretization must be 'rotation' or 'shear'")
-    _check(lib().o1d_make_taps_ex(K, pad, C, _ptr(a), TAPS[discretization], _ptr(oh), _ptr(ow)))
+        raise ValueError("discretization must be 'rotation', 'shear' or 'bilinear'")
+    _check(lib().o1d_make_taps_ex(K, float(pad), C, _ptr(a), TAPS[discretization], _ptr(oh), _ptr(ow)))
     return oh, ow
+
+
+def make_bilinear(K: int, angles_deg, pad: float = -1):
+    """Bilinear taps: base corners h0, w0 int16 [C][K] and fractional parts
+    fa, fb float64 [C][K] of the real offsets (-(k-pad) sin t, (k-pad) cos t)."""
+    a = np.ascontiguousarray(angles_deg, dtype=np.float64)
+    C = a.shape[0]
+    h0, w0 = np.empty((C, K), np.int16), np.empty((C, K), np.int16)
+    fa, fb = np.empty((C, K), np.float64), np.empty((C, K), np.float64)
+    _check(lib().o1d_make_bilinear(K, float(pad), C, _ptr(a), _ptr(h0), _ptr(w0), _ptr(fa), _ptr(fb)))
+    return h0, w0, fa, fb
 
 
 def direction_angles(D: int, C: int, assign: str = "contiguous", shift_deg: float = 0.0) -> np.ndarray:
@@ -121,10 +139,11 @@ def direction_angles(D: int, C: int, assign: str = "contiguous", shift_deg: floa
     return out
 
 
-def spec_source(N, C, H, W, K, angles_deg, pass_id: int, stride=1, pad=-1, dtype=torch.float32) -> str:
-    """CUDA source of the specialised kernel for one pass (host only, diagnostics)."""
+def spec_source(N, C, H, W, K, angles_deg, pass_id: int, stride=1, pad=-1, dtype=torch.float32, flags=0) -> str:
+    """CUDA source of the specialised kernel for one pass (0 fwd, 1 bwd_in, 2 bwd_w, 3 fused
+    backward; host only, diagnostics)."""
     a = np.ascontiguousarray(angles_deg, dtype=np.float64)
-    d = _Desc(N, C, H, W, K, stride, pad, DTYPES[dtype], 0, 0)
+    d = _Desc(N, C, H, W, K, stride, float(pad), DTYPES[dtype], 0, flags)
     n = ctypes.c_size_t(0)
     _check(lib().o1d_spec_source(ctypes.byref(d), _ptr(a), pass_id, None, ctypes.byref(n)))
     buf = ctypes.create_string_buffer(n.value)
@@ -143,9 +162,11 @@ class Plan:
     def __init__(self, N, C, H, W, K, angles_deg, stride=1, pad=-1, dtype=torch.float32, flags=0, device=None,
                  discretization="rotation"):
         if discretization not in TAPS:
-            raise ValueError("discretization must be 'rotation' or 'shear'")
+            raise ValueError("discretization must be 'rotation', 'shear' or 'bilinear'")
         if discretization == "shear":
             flags |= FLAG_SHEAR
+        if discretization == "bilinear":
+            flags |= FLAG_BILINEAR
         a = np.ascontiguousarray(angles_deg, dtype=np.float64)
         if a.shape != (C,):
             raise ValueError("angles must have shape [C]")
@@ -156,7 +177,7 @@ class Plan:
         self.angles = a
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.device = dev
-        d = _Desc(N, C, H, W, K, stride, pad, DTYPES[dtype], 0, flags)
+        d = _Desc(N, C, H, W, K, stride, float(pad), DTYPES[dtype], 0, flags)
         h = ctypes.c_void_p()
         with torch.cuda.device(dev):
             _check(lib().o1d_plan_create(ctypes.byref(d), _ptr(a), ctypes.byref(h)))
@@ -165,6 +186,7 @@ class Plan:
         _check(lib().o1d_plan_out_shape(h, ctypes.byref(P), ctypes.byref(Q)))
         self.P, self.Q = P.value, Q.value
         self.pad = K // 2 if pad < 0 else pad
+        self.discretization = discretization
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -193,6 +215,12 @@ class Plan:
             return np.zeros((0, 2), np.uint64)
         rec = buf[1:].reshape(-1, 2)
         return rec[rec[:, 0] != 0]
+
+    def stats(self):
+        """(plan-creation host ms, JIT module-cache hit: 1 / 0, -1 = no specialised kernels)."""
+        ms, hit = ctypes.c_double(), ctypes.c_int32()
+        _check(lib().o1d_plan_stats(self._h, ctypes.byref(ms), ctypes.byref(hit)))
+        return ms.value, hit.value
 
     def workspace_bytes(self) -> int:
         return int(lib().o1d_workspace_bytes(self._h))
@@ -263,6 +291,21 @@ def backward_weight(plan: Plan, x, dy, dW=None, ws=None, stream=None):
     return dW
 
 
+def backward(plan: Plan, x, dy, w, dx=None, dW=None, ws=None, stream=None):
+    """backward_input and backward_weight in one pass over x and dy (o1d_backward, NEXT-2)."""
+    _check_tensor(x, "x", plan.x_shape(), plan.dtype, plan.device)
+    _check_tensor(dy, "dy", plan.y_shape(), plan.dtype, plan.device)
+    _check_tensor(w, "w", (plan.C, plan.K), torch.float32, plan.device)
+    dx = torch.empty(plan.x_shape(), dtype=plan.dtype, device=plan.device) if dx is None else dx
+    dW = torch.empty((plan.C, plan.K), dtype=torch.float32, device=plan.device) if dW is None else dW
+    _check_tensor(dx, "dx", plan.x_shape(), plan.dtype, plan.device)
+    _check_tensor(dW, "dW", (plan.C, plan.K), torch.float32, plan.device)
+    ws = workspace(plan) if ws is None else ws
+    _check(lib().o1d_backward(plan.handle, x.data_ptr(), dy.data_ptr(), w.data_ptr(), dx.data_ptr(), dW.data_ptr(),
+                              ws.data_ptr(), ws.numel() * ws.element_size(), _stream_handle(stream)))
+    return dx, dW
+
+
 def step(plan: Plan, x, w, dy, y=None, dx=None, dW=None, ws=None, stream=None):
     """One layer training step on device tensors (o1d_step): forward, backward_input and
     backward_weight with the later passes overlapping the earlier ones' tails."""
@@ -303,4 +346,6 @@ o1d_plan_create = plan_create
 o1d_forward = forward
 o1d_backward_input = backward_input
 o1d_backward_weight = backward_weight
+o1d_backward = backward
+o1d_make_bilinear = make_bilinear
 o1d_step_host = step_host

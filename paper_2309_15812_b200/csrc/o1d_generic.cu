@@ -1,7 +1,9 @@
 // o1d_generic.cu — runtime-tap ("generic") kernels of liboriented1d.
 //
 // These kernels take the tap table at run time, so they serve every plan
-// (arbitrary per-channel angles, any K, any stride).  They stage the input band
+// (arbitrary per-channel angles, any K, any stride, every discretisation: the
+// plan's expanded weighted taps (dh, dw, k, coef) -- one per tap for the
+// rotation / shear forms, up to four per tap for bilinear interpolation).  They stage the input band
 // plus the angle-dependent halo in shared memory once (zero-filled outside the
 // image: reading R1), so every tap read is a shared-memory read — the paper's
 // "load the whole input in shared GPU memory ... cut the image into bands"
@@ -38,14 +40,15 @@ struct StencilArgs {
     const void *in;
     const float *w;
     void *out;
-    const int16_t *dh, *dw;
-    int C, Hi, Wi, Ho, Wo, str, K;
+    const int16_t *dh, *dw, *ek;
+    const float *coef;
+    int C, Hi, Wi, Ho, Wo, str, K, KE;
     int minDH, maxDH, minDW;
     int band, bands;
     int tileRows, tileCols, pitch;
 };
 
-// out[p][q] = sum_k in[str*p + dh_k][str*q + dw_k] * w_k, one CTA per (plane, band of output rows)
+// out[p][q] = sum_e in[str*p + dh_e][str*q + dw_e] * coef_e * w_{k_e}, one CTA per (plane, band of output rows)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a) {
     extern __shared__ float sm[];
@@ -57,10 +60,11 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     const int nrows = min(a.band, a.Ho - p0);
     float *tile = sm;
     int *toff = reinterpret_cast<int *>(tile + a.tileRows * a.pitch + 8 * a.str + a.pitch);
-    float *wk = reinterpret_cast<float *>(toff + a.K);
-    for (int k = tid; k < a.K; k += blockDim.x) {
-        toff[k] = (a.dh[c * a.K + k] - a.minDH) * a.pitch + (a.dw[c * a.K + k] - a.minDW);
-        wk[k] = a.w[c * a.K + k];
+    float *wk = reinterpret_cast<float *>(toff + a.KE);
+    for (int e = tid; e < a.KE; e += blockDim.x) {
+        const int i = c * a.KE + e;
+        toff[e] = (a.dh[i] - a.minDH) * a.pitch + (a.dw[i] - a.minDW);
+        wk[e] = a.coef[i] * a.w[c * a.K + a.ek[i]];
     }
     const T *in = static_cast<const T *>(a.in) + (size_t)plane * a.Hi * a.Wi;
     const int h0 = a.str * p0 + a.minDH;
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
         const int pr = g / qg, q0 = (g - pr * qg) * 4;
         const float *base = tile + pr * a.str * a.pitch + q0 * a.str;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-        for (int k = 0; k < a.K; ++k) {
+        for (int k = 0; k < a.KE; ++k) {
             const float *s = base + toff[k];
             const float wv = wk[k];
             acc0 = fmaf(s[0], wv, acc0);
@@ -93,12 +97,13 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     }
 }
 
-// dx[h][w] = sum_k [str | h-oh_k, str | w-ow_k, in range] dy[(h-oh_k)/str][(w-ow_k)/str] * w_k
+// dx[h][w] = sum_e [str | h-oh_e, str | w-ow_e, in range] dy[(h-oh_e)/str][(w-ow_e)/str] * coef_e * w_{k_e}
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_input_strided_kernel(const T *dy, const float *w, T *dx,
                                                                      const int16_t *oh, const int16_t *ow,
+                                                                     const int16_t *ek, const float *coef,
                                                                      int C, int H, int W, int P, int Q, int K,
-                                                                     int str, long total) {
+                                                                     int KE, int str, long total) {
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const int v = (int)(i % W);
@@ -107,12 +112,13 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_kernel(const T *dy
     const int c = (int)(plane % C);
     const T *g = dy + plane * P * Q;
     float acc = 0.f;
-    for (int k = 0; k < K; ++k) {
-        const int a = h - oh[c * K + k], b = v - ow[c * K + k];
+    for (int e = 0; e < KE; ++e) {
+        const int i = c * KE + e;
+        const int a = h - oh[i], b = v - ow[i];
         if (a < 0 || b < 0 || a % str || b % str) continue;
         const int p = a / str, q = b / str;
         if (p >= P || q >= Q) continue;
-        acc = fmaf(ld_act<T>(g + p * Q + q), w[c * K + k], acc);
+        acc = fmaf(ld_act<T>(g + p * Q + q), coef[i] * w[c * K + ek[i]], acc);
     }
     dx[i] = to_act<T>(acc);
 }
@@ -121,7 +127,7 @@ struct BwdWArgs {
     const void *x, *dy;
     float *ws;
     const int16_t *oh, *ow;
-    int C, H, W, P, Q, str, K;
+    int C, H, W, P, Q, str, K;   // K here: expanded taps per channel (KE)
     int minOH, maxOH, minOW;
     int band, bands;
     int tileRows, tileCols, pitch;
@@ -143,7 +149,7 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
     return v[0];
 }
 
-// ws[plane*bands + band][k] = sum over the band's outputs of dy[p][q] * x[str*p+oh_k][str*q+ow_k]
+// ws[plane*bands + band][e] = sum over the band's outputs of dy[p][q] * x[str*p+oh_e][str*q+ow_e] (expanded taps)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a) {
     extern __shared__ float sm[];
@@ -196,15 +202,22 @@ __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a
     }
 }
 
-// dW[c][k] = sum_n sum_band ws[(n*C + c)*bands + band][k], f64 accumulation, fixed order
-__global__ void bwd_weight_finalize_kernel(const float *ws, float *dW, int N, int C, int K, int bands) {
+// dW[c][k] = sum_{e: k_e = k} coef_e * (sum_n sum_band ws[(n*C + c)*bands + band][e]), f64 accumulation,
+// fixed order (rotation / shear: one e per k with coef 1)
+__global__ void bwd_weight_finalize_kernel(const float *ws, float *dW, const int16_t *ek, const float *coef, int N,
+                                           int C, int K, int KE, int bands) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= C * K) return;
     const int c = i / K, k = i - c * K;
-    double s = 0.0;
-    for (int n = 0; n < N; ++n)
-        for (int b = 0; b < bands; ++b) s += (double)ws[((size_t)(n * C + c) * bands + b) * K + k];
-    dW[i] = (float)s;
+    double acc = 0.0;
+    for (int e = 0; e < KE; ++e) {
+        if (ek[c * KE + e] != k || coef[c * KE + e] == 0.0f) continue;
+        double s = 0.0;
+        for (int n = 0; n < N; ++n)
+            for (int b = 0; b < bands; ++b) s += (double)ws[((size_t)(n * C + c) * bands + b) * KE + e];
+        acc += (double)coef[c * KE + e] * s;
+    }
+    dW[i] = (float)acc;
 }
 
 o1d_status check_launch(const char *what) {
@@ -234,7 +247,7 @@ void tile_geometry(const Stencil &st, int band, int *rows, int *cols, int *pitch
 size_t stencil_smem(const Stencil &st, int band, int extra_rows_per_out) {
     int rows, cols, pitch;
     tile_geometry(st, band, &rows, &cols, &pitch);
-    return sizeof(float) * ((size_t)rows * pitch + 8 * st.str + pitch + 2 * st.K +
+    return sizeof(float) * ((size_t)rows * pitch + 8 * st.str + pitch + 2 * st.KE +
                             (size_t)extra_rows_per_out * band * st.Wo);
 }
 
@@ -252,8 +265,8 @@ int generic_band_rows(const o1d_plan *, const Stencil &st, int extra) {
 o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, const void *in, const float *w,
                            void *out, void *stream) {
     StencilArgs a;
-    a.in = in; a.w = w; a.out = out; a.dh = st.d_dh; a.dw = st.d_dw;
-    a.C = pl->d.C; a.Hi = st.Hi; a.Wi = st.Wi; a.Ho = st.Ho; a.Wo = st.Wo; a.str = st.str; a.K = st.K;
+    a.in = in; a.w = w; a.out = out; a.dh = st.d_dh; a.dw = st.d_dw; a.ek = pl->d_ek; a.coef = pl->d_coef;
+    a.C = pl->d.C; a.Hi = st.Hi; a.Wi = st.Wi; a.Ho = st.Ho; a.Wo = st.Wo; a.str = st.str; a.K = pl->d.K; a.KE = st.KE;
     a.minDH = st.minDH; a.maxDH = st.maxDH; a.minDW = st.minDW;
     a.band = band; a.bands = (st.Ho + band - 1) / band;
     tile_geometry(st, band, &a.tileRows, &a.tileCols, &a.pitch);
@@ -278,8 +291,8 @@ o1d_status generic_bwd_input_strided(const o1d_plan *pl, const void *dy, const f
     return dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
         using T = decltype(tag);
         bwd_input_strided_kernel<T><<<grid, kThreads, 0, s>>>(static_cast<const T *>(dy), w, static_cast<T *>(dx),
-                                                              pl->d_oh, pl->d_ow, d.C, d.H, d.W, pl->P, pl->Q,
-                                                              d.K, d.stride, total);
+                                                              pl->d_oh, pl->d_ow, pl->d_ek, pl->d_coef, d.C, d.H,
+                                                              d.W, pl->P, pl->Q, d.K, pl->KE, d.stride, total);
         return check_launch("bwd_input_strided");
     });
 }
@@ -290,11 +303,11 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
     const Stencil &st = pl->fwd;
     BwdWArgs a;
     a.x = x; a.dy = dy; a.ws = ws; a.oh = pl->d_oh; a.ow = pl->d_ow;
-    a.C = d.C; a.H = d.H; a.W = d.W; a.P = pl->P; a.Q = pl->Q; a.str = d.stride; a.K = d.K;
+    a.C = d.C; a.H = d.H; a.W = d.W; a.P = pl->P; a.Q = pl->Q; a.str = d.stride; a.K = pl->KE;
     a.minOH = st.minDH; a.maxOH = st.maxDH; a.minOW = st.minDW;
     a.band = pl->bw_band; a.bands = pl->bw_bands;
     tile_geometry(st, a.band, &a.tileRows, &a.tileCols, &a.pitch);
-    const size_t smem = sizeof(float) * ((size_t)a.tileRows * a.pitch + (size_t)a.band * a.Q + d.K);
+    const size_t smem = sizeof(float) * ((size_t)a.tileRows * a.pitch + (size_t)a.band * a.Q + pl->KE);
     const long grid = (long)d.N * d.C * a.bands;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     o1d_status r = dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
@@ -307,7 +320,8 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
     });
     if (r != O1D_OK) return r;
     const int n = d.C * d.K;
-    bwd_weight_finalize_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, dW, d.N, d.C, d.K, a.bands);
+    bwd_weight_finalize_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, dW, pl->d_ek, pl->d_coef, d.N, d.C, d.K, pl->KE,
+                                                               a.bands);
     return check_launch("bwd_weight_finalize");
 }
 

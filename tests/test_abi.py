@@ -60,11 +60,26 @@ def test_make_taps_bit_exact_vs_oracle(K):
 
 
 def test_make_taps_nondefault_pad():
-    angles = np.array([0.0, 22.5, 45.0, 90.0, 135.0, 300.0])
-    for K, pad in ((7, 0), (7, 6), (8, 4), (6, 2)):
+    angles = np.array([0.0, 22.5, 30.0, 45.0, 60.0, 90.0, 135.0, 150.0, 300.0, 17.3])
+    for K, pad in ((7, 0), (7, 6), (8, 4), (6, 2), (6, 2.5), (7, 1.25), (31, 14.5), (4, 0.5)):
         oh, ow = B.make_taps(K, angles, pad=pad)
         roh, row = T.taps_table(K, pad, angles)
-        assert np.array_equal(oh, np.array(roh)) and np.array_equal(ow, np.array(row))
+        assert np.array_equal(oh, np.array(roh)) and np.array_equal(ow, np.array(row)), (K, pad)
+
+
+@pytest.mark.parametrize("K", [3, 7, 15, 31])
+def test_make_bilinear_vs_oracle(K):
+    """Bilinear tables: base corners bit-exact, fractional parts within 1e-14 of
+    the oracle's 80-digit values (exactly 0 / 1/2 at the Niven angles)."""
+    sets = _angle_sets()
+    for name in ("D8_cycled", "D=C=96", "integer_deg", "near_niven", "big"):
+        angles = sets[name]
+        h0, w0, fa, fb = B.make_bilinear(K, np.array(angles))
+        rh, rw, ra, rb = (np.array(v) for v in T.bilinear_table(K, K // 2, angles))
+        assert np.array_equal(h0, rh) and np.array_equal(w0, rw), name
+        assert np.max(np.abs(fa - ra)) < 1e-14 and np.max(np.abs(fb - rb)) < 1e-14, name
+        exact = np.isin(np.array(angles) % 360.0, [0.0, 30.0, 90.0, 150.0, 180.0, 210.0, 270.0, 330.0])
+        assert np.array_equal(fa[exact], ra[exact]), name
 
 
 def test_direction_angles_vs_oracle():
@@ -88,7 +103,11 @@ def test_error_codes():
     for fields, status in (((0, 4, 8, 8, 3, 1, -1, 0, 0, 0), 2),  # N = 0
                            ((1, 4, 8, 8, 0, 1, -1, 0, 0, 0), 3),  # K = 0
                            ((1, 4, 8, 8, 3, 0, -1, 0, 0, 0), 3),  # stride 0
-                           ((1, 4, 8, 8, 3, 1, 3, 0, 0, 0), 3),   # pad >= K
+                           ((1, 4, 8, 8, 3, 1, 3, 0, 0, 0), 3),   # pad > K - 1
+                           ((1, 4, 8, 8, 3, 1, 2.5, 0, 0, 0), 3),  # pad > K - 1 (real)
+                           ((1, 4, 8, 8, 3, 1, float("nan"), 0, 0, 0), 1),  # non-finite pad
+                           ((1, 4, 8, 8, 3, 1, 1.5, 0, 0, 4), 5),  # shear with a non-integer pad
+                           ((1, 4, 8, 8, 3, 1, -1, 0, 0, 12), 3),  # shear and bilinear
                            ((1, 4, 8, 8, 3, 1, -1, 7, 0, 0), 5),  # dtype
                            ((1, 4, 8, 8, 3, 1, -1, 0, 1, 0), 5)):  # layout
         d = B._Desc(*fields)
@@ -98,14 +117,17 @@ def test_error_codes():
     assert L.o1d_forward(None, None, None, None, None) == 1
 
 
-@pytest.mark.parametrize("pass_id", [0, 1, 2])
-def test_spec_source_compiles_for_sm100a(tmp_path, pass_id):
+@pytest.mark.parametrize("disc", ["rotation", "bilinear"])
+@pytest.mark.parametrize("pass_id", [0, 1, 2, 3])
+def test_spec_source_compiles_for_sm100a(tmp_path, pass_id, disc):
     """The runtime-generated specialised kernels are valid sm_100a CUDA (host-only
-    generation through the ABI, compiled here with nvcc; no GPU needed)."""
+    generation through the ABI, compiled here with nvcc; no GPU needed); pass 3 is the
+    fused backward (NEXT-2)."""
     import shutil
     import subprocess
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    src = B.spec_source(2, 16, 56, 56, 15, T.direction_angles(8, 16, "cycled"), pass_id)
+    flags = B.FLAG_BILINEAR if disc == "bilinear" else 0
+    src = B.spec_source(2, 16, 56, 56, 15, T.direction_angles(8, 16, "cycled"), pass_id, flags=flags)
     assert "o1d_" in src and "cp.async.bulk.tensor" in src
     f = tmp_path / f"k{pass_id}.cu"
     f.write_text(src)
@@ -113,9 +135,9 @@ def test_spec_source_compiles_for_sm100a(tmp_path, pass_id):
                         str(f)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
     sass = subprocess.run(["cuobjdump", "-sass", str(tmp_path / "k.cubin")], capture_output=True, text=True).stdout
-    assert "UTMALDG" in sass  # TMA tile loads
-    if pass_id < 2:
-        assert "FFMA2" in sass and "UTMASTG" in sass  # packed FP32 + TMA stores
+    assert "UTMALDG" in sass and "FFMA2" in sass  # TMA tile loads, packed FP32
+    if pass_id != 2:
+        assert "UTMASTG" in sass  # TMA band stores
 
 
 def test_spec_source_ineligible_shapes():
@@ -140,7 +162,7 @@ def test_make_taps_shear_bit_exact():
         roh, row = T.taps_table(K, K // 2, angs, "shear")
         assert np.array_equal(oh, np.array(roh)) and np.array_equal(ow, np.array(row)), K
     with pytest.raises(ValueError):
-        B.make_taps(7, np.zeros(2), discretization="bilinear")
+        B.make_taps(7, np.zeros(2), discretization="nonsense")
     import ctypes
     a = np.zeros(2)
     o1, o2 = np.empty((2, 7), np.int16), np.empty((2, 7), np.int16)

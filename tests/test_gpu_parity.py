@@ -26,26 +26,44 @@ def nerr(g: torch.Tensor, r: np.ndarray) -> float:
 _oracle_cache = {}
 
 
+def oracle_case(N, C, H, W, K, angles, stride, dt, disc, x, w, dy, threads=None):
+    """(oh, ow, y, dx, dW) of the oracle on these inputs (cached for the last key)."""
+    key = (N, C, H, W, K, tuple(angles), stride, dt, disc)
+    if key not in _oracle_cache:
+        th = threads or max(1, oracle.max_threads())
+        _oracle_cache.clear()
+        if disc == "bilinear":
+            h0, w0, fa, fb = (np.array(v) for v in T.bilinear_table(K, K // 2, angles))
+            oh, ow = h0.astype(np.int32), w0.astype(np.int32)
+            _oracle_cache[key] = (oh, ow, oracle.forward_bilinear(x, w, h0, w0, fa, fb, stride, th),
+                                  oracle.backward_input_bilinear(dy, w, h0, w0, fa, fb, H, W, stride, th),
+                                  oracle.backward_weight_bilinear(x, dy, h0, w0, fa, fb, stride, th))
+        else:
+            oh, ow = T.taps_table(K, K // 2, angles, disc)
+            oh, ow = np.array(oh, np.int32), np.array(ow, np.int32)
+            _oracle_cache[key] = (oh, ow, oracle.forward(x, w, oh, ow, stride, th),
+                                  oracle.backward_input(dy, w, oh, ow, H, W, stride, th),
+                                  oracle.backward_weight(x, dy, oh, ow, stride, th))
+    return _oracle_cache[key]
+
+
 def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, threads=None, check_det=False,
-             disc="rotation"):
+             disc="rotation", expect=None):
+    """All passes (forward, backward_input, backward_weight and the fused o1d_backward) vs the
+    oracle; `expect`: "spec" / "generic" = the kernel family the plan must select."""
     angles = [float(a) for a in angles]
     plan = B.Plan(N, C, H, W, K, np.array(angles), stride=stride, dtype=dtype, flags=flags, device="cuda:0",
                   discretization=disc)
+    if expect == "spec":
+        assert plan.describe().startswith("spec"), plan.describe()
+    elif expect == "generic":
+        assert plan.describe().startswith("generic"), plan.describe()
     P, Q = plan.P, plan.Q
     dt = NP_DT[dtype]
     x = inputs.activation((N, C, H, W), 0, dt)
     w = inputs.weights(C, K, 1)
     dy = inputs.activation((N, C, P, Q), 2, dt)
-    key = (N, C, H, W, K, tuple(angles), stride, dt, disc)
-    if key not in _oracle_cache:
-        oh, ow = T.taps_table(K, K // 2, angles, disc)
-        oh, ow = np.array(oh, np.int32), np.array(ow, np.int32)
-        th = threads or max(1, oracle.max_threads())
-        _oracle_cache.clear()
-        _oracle_cache[key] = (oh, ow, oracle.forward(x, w, oh, ow, stride, th),
-                              oracle.backward_input(dy, w, oh, ow, H, W, stride, th),
-                              oracle.backward_weight(x, dy, oh, ow, stride, th))
-    oh, ow, ry, rdx, rdW = _oracle_cache[key]
+    oh, ow, ry, rdx, rdW = oracle_case(N, C, H, W, K, angles, stride, dt, disc, x, w, dy, threads)
     poh, pow_ = plan.taps()
     assert np.array_equal(poh, oh) and np.array_equal(pow_, ow), "tap tables must be bit-exact"
     tx = torch.from_numpy(x).to("cuda:0", dtype)
@@ -54,10 +72,13 @@ def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, thre
     y = B.forward(plan, tx, tw)
     dx = B.backward_input(plan, tdy, tw)
     dW = B.backward_weight(plan, tx, tdy)
+    fdx, fdW = B.backward(plan, tx, tdy, tw)
     torch.cuda.synchronize()
     errs = {"y": nerr(y, ry), "dx": nerr(dx, rdx), "dW": nerr(dW, rdW)}
     tol = TOL[dtype]
     assert all(e <= tol for e in errs.values()), (plan.describe(), errs)
+    # the fused backward (NEXT-2) computes the same partial sums in the same order: bitwise
+    assert torch.equal(fdx, dx) and torch.equal(fdW, dW), plan.describe()
     if check_det:
         y2 = B.forward(plan, tx, tw)
         dx2 = B.backward_input(plan, tdy, tw)
@@ -254,17 +275,6 @@ def test_repeated_launches_bitwise():
     assert not bad, f"steps with different results: {sorted(set(bad))[:20]}"
 
 
-@pytest.mark.parametrize("v2", ["0", "1", "2"])
-def test_pipeline_variants(v2, monkeypatch):
-    """The v1 pipeline (two tap groups, 3 CTAs/SM) stays a tested fallback: O1D_V2 selects
-    per pass (bit 1 stencils, bit 2 backward_weight) at plan creation."""
-    monkeypatch.setenv("O1D_V2", v2)
-    plan, errs = run_case(2, 16, 56, 56, 31, T.direction_angles(8, 16, "cycled"), 1, torch.float32, 0,
-                          check_det=True)
-    assert "spec" in plan.describe()
-
-
-
 @pytest.mark.parametrize("flags", sorted(FLAGS))
 @pytest.mark.parametrize("HW", [(56, 56), (37, 48), (14, 14)])
 @pytest.mark.parametrize("stride", [1, 2])
@@ -305,7 +315,7 @@ def test_step_host_pipelined_bitwise(chunks, monkeypatch):
     monkeypatch.setenv("O1D_E2E_CHUNKS", chunks)
     angles = T.direction_angles(8, 16, "cycled")
     plan = B.Plan(8, 16, 56, 56, 31, np.array(angles), device="cuda:0")
-    assert "spec-v2" in plan.describe()
+    assert plan.describe().startswith("spec")
     x = torch.from_numpy(inputs.activation(plan.x_shape(), 0)).pin_memory()
     w = torch.from_numpy(inputs.weights(16, 31)).pin_memory()
     dy = torch.from_numpy(inputs.activation(plan.y_shape(), 2)).pin_memory()
@@ -337,3 +347,148 @@ def test_step_api_bitwise_and_repeated():
         if i % 25 == 24:
             torch.cuda.synchronize()
             assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0), i
+
+
+# ---------------------------------------------------------------------------------------
+# Angle sets, assignments and strides at SPEC-ELIGIBLE shapes (the JIT kernels), VERDICT r1
+# item 1(a)/(b): every test asserts which kernel family ran.
+SPEC_SETS = {
+    # <= 16 distinct tables of the D=C 30-degree family (Niven angles: exact floors matter)
+    "thirties_16": [i * 180.0 / 96 for i in range(0, 96, 6)],
+    "thirties_exact": [0.0, 30.0, 60.0, 90.0, 120.0, 150.0, 210.0, 330.0],
+    "integer_deg": [float((37 * c) % 360) for c in range(16)],
+    "near_90": [89.999, 90.001, 89.9999999, 90.0000001, 0.001, -0.001, 179.999, 45.0],
+    "neg_and_big": [-30.0, 725.5, -3600.0, 1e3, -1e5 - 30.0, 1e6 + 0.5, 180.0, 270.0],
+}
+
+
+@pytest.mark.parametrize("HW", [(56, 56), (40, 48)])
+@pytest.mark.parametrize("K", [15, 31])
+@pytest.mark.parametrize("angle_set", sorted(SPEC_SETS))
+def test_angle_sets_spec(angle_set, K, HW):
+    angles = SPEC_SETS[angle_set]
+    C = 16
+    angles = [angles[c % len(angles)] for c in range(C)]
+    H, W = HW
+    run_case(2, C, H, W, K, angles, 1, torch.float32, 0, expect="spec")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("assign", ["contiguous", "cycled"])
+def test_assignments_spec(assign, dtype):
+    # the model harness uses the paper's contiguous groups
+    run_case(2, 16, 56, 56, 31, T.direction_angles(8, 16, assign), 1, dtype, 0, check_det=True, expect="spec")
+
+
+def test_full_stage1_contiguous():
+    wl = inputs.S1
+    run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, "contiguous"), 1, torch.float32, 0,
+             expect="spec")
+
+
+def test_full_stage1_stride2():
+    """S1 at stride 2: the generic kernels (strided gather for dx)."""
+    wl = inputs.S1
+    run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 2, torch.float32, 0,
+             expect="generic")
+
+
+def test_full_ksweep_bf16():
+    wl = inputs.ksweep(31)
+    run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, torch.bfloat16, 0)
+
+
+# ---------------------------------------------------------------------------------------
+# Bilinear discretisation (NEXT-4, P:309-311): the JIT kernels take weighted taps (each tap
+# split over its four neighbours), the generic kernels the expanded table.
+@pytest.mark.parametrize("flags", sorted(FLAGS))
+@pytest.mark.parametrize("HW", [(56, 56), (37, 45), (14, 14)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_bilinear(flags, HW, stride):
+    H, W = HW
+    angles = T.direction_angles(8, 16, "cycled") if stride == 1 else [17.0, 30.0, 63.5, 90.0, 100.0, 135.0, 170.0, 225.0]
+    C = len(angles) if stride != 1 else 16
+    K = 15 if stride == 1 else 7
+    run_case(2, C, H, W, K, angles, stride, torch.float32, FLAGS[flags], check_det=True, disc="bilinear")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_bilinear_full_stage1(dtype):
+    wl = inputs.S1
+    run_case(wl.N, wl.C, wl.H, wl.W, wl.K, T.direction_angles(wl.D, wl.C, wl.assign), 1, dtype, 0,
+             disc="bilinear", expect="spec")
+
+
+# ---------------------------------------------------------------------------------------
+def test_plan_module_cache_and_batch_independence():
+    """The generated source does not depend on N: a second plan with another batch size (or a
+    re-created plan) reuses the compiled modules; its results match the oracle."""
+    angles = np.array(T.direction_angles(8, 16, "cycled"))
+    p1 = B.Plan(4, 16, 56, 56, 31, angles, device="cuda:0")
+    ms1, hit1 = p1.stats()
+    p2 = B.Plan(3, 16, 56, 56, 31, angles, device="cuda:0")
+    ms2, hit2 = p2.stats()
+    assert hit2 == 1 and "module cache hit" in p2.describe(), p2.describe()
+    run_case(3, 16, 56, 56, 31, angles, 1, torch.float32, 0, expect="spec")
+
+
+def test_step_fused_bitwise(monkeypatch):
+    """o1d_step with the fused backward (O1D_FUSED=1 at plan creation) gives bitwise the three
+    separate calls' results, step after step (the persistent kernels' slots reset)."""
+    monkeypatch.setenv("O1D_FUSED", "1")
+    wl = inputs.S1
+    angles = T.direction_angles(wl.D, wl.C, wl.assign)
+    plan = B.Plan(16, wl.C, wl.H, wl.W, wl.K, np.array(angles), device="cuda:0")
+    assert "step=fused" in plan.describe(), plan.describe()
+    g = torch.Generator(device="cuda:0").manual_seed(2)
+    x = torch.rand(16, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    dy = torch.rand(16, wl.C, wl.H, wl.W, device="cuda:0", generator=g)
+    w = torch.rand(wl.C, wl.K, device="cuda:0", generator=g)
+    y0, dx0, dW0 = B.forward(plan, x, w), B.backward_input(plan, dy, w), B.backward_weight(plan, x, dy)
+    ws = B.workspace(plan)
+    y, dx, dW = torch.empty_like(y0), torch.empty_like(dx0), torch.empty_like(dW0)
+    for i in range(100):
+        B.step(plan, x, w, dy, y, dx, dW, ws)
+        if i % 25 == 24:
+            torch.cuda.synchronize()
+            assert torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0), i
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_step_host_full_width_windows(fused, monkeypatch):
+    """Batch windows of a full-width plan (C=96, N=8: 1-2 planes per table per window, every
+    CTA's home table exhausted early): every item is computed once whatever SMs the CTAs land
+    on (the scheduler's cross-table stealing)."""
+    monkeypatch.setenv("O1D_E2E_CHUNKS", "8")
+    monkeypatch.setenv("O1D_FUSED", fused)
+    angles = T.direction_angles(8, 96, "cycled")
+    plan = B.Plan(8, 96, 56, 56, 31, np.array(angles), device="cuda:0")
+    x = torch.from_numpy(inputs.activation(plan.x_shape(), 0)).pin_memory()
+    w = torch.from_numpy(inputs.weights(96, 31)).pin_memory()
+    dy = torch.from_numpy(inputs.activation(plan.y_shape(), 2)).pin_memory()
+    y, dx, dW = torch.empty_like(x).pin_memory(), torch.empty_like(x).pin_memory(), torch.empty_like(w).pin_memory()
+    xd, wd, dyd = x.cuda(), w.cuda(), dy.cuda()
+    ry, rdx, rdW = B.forward(plan, xd, wd).cpu(), B.backward_input(plan, dyd, wd).cpu(), B.backward_weight(plan, xd, dyd).cpu()
+    for _ in range(3):
+        B.step_host(plan, x, w, dy, y, dx, dW, B.step_host_workspace(plan))
+        assert torch.equal(y, ry) and torch.equal(dx, rdx) and torch.equal(dW, rdW)
+
+
+def test_torch_library_opcheck():
+    """The o1d::* custom ops (schema, fake/meta implementations, autograd registration)
+    pass torch.library.opcheck; the module's autograd uses the fused backward op."""
+    from paper_2309_15812_b200 import module as M
+    angles = np.array(T.direction_angles(8, 16, "cycled"))
+    plan = B.Plan(2, 16, 56, 56, 31, angles, device="cuda:0")
+    pid = M.register_plan(plan)
+    x = torch.randn(2, 16, 56, 56, device="cuda:0", requires_grad=True)
+    w = torch.randn(16, 31, device="cuda:0", requires_grad=True)
+    dy = torch.randn(2, 16, 56, 56, device="cuda:0")
+    torch.library.opcheck(torch.ops.o1d.forward.default, (x, w, pid))
+    torch.library.opcheck(torch.ops.o1d.backward_input.default, (dy, w.detach(), pid))
+    torch.library.opcheck(torch.ops.o1d.backward_weight.default, (x.detach(), dy, pid))
+    torch.library.opcheck(torch.ops.o1d.backward.default, (x.detach(), dy, w.detach(), pid))
+    y = M.oriented1d_dwconv(x, w, plan)
+    y.backward(dy)
+    assert torch.equal(x.grad, B.backward_input(plan, dy, w.detach()))
+    assert torch.equal(w.grad, B.backward_weight(plan, x.detach(), dy))
