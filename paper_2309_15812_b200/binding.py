@@ -201,6 +201,12 @@ class Plan:
     def describe(self) -> str:
         return lib().o1d_plan_describe(self._h).decode()
 
+    @property
+    def fused_step(self) -> bool:
+        """o1d_step / the module's autograd use the fused single-pass backward (O1D_FUSED=1 at
+        plan creation); otherwise backward_input + backward_weight."""
+        return "step=fused" in self.describe()
+
     def taps(self):
         oh = np.empty((self.C, self.K), np.int16)
         ow = np.empty((self.C, self.K), np.int16)

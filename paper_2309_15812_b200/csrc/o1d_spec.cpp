@@ -286,6 +286,8 @@ struct SpecSet {
     size_t smem[kPasses] = {0, 0, 0, 0};
     int grid[kPasses] = {0, 0, 0, 0}, threads[kPasses] = {0, 0, 0, 0};
     bool pdl = true;                     // programmatic dependent launch (O1D_PDL at plan creation)
+    std::string src3;                    // fused backward source, compiled on first use
+    std::mutex mu3;
     // work-queue counters: kPasses x kSlots launch slots x (NT next counters + 1 done counter);
     // every launch takes the next slot (host atomic), so concurrent launches on different
     // streams never share counters; a slot is reset by the last producer warp of its launch
@@ -313,7 +315,16 @@ struct Params {
   u64* trace;        // diagnostics (O1D_TRACE): [0] = record count, then (globaltimer, tag) pairs
   int N, n0, nlen;   // batch size; batch window [n0, n0 + nlen) (nlen = 0: all)
   int nowait;        // 1: no griddepcontrol.wait before the loads (o1d_step: inputs not from the predecessor)
+  const void* cvt1;  // 16-bit plans: ring-1 planes (x or dy) widened to fp32 by the producers
+  const void* cvt2;  // 16-bit fused plans: ring-2 planes (dy)
 };
+// streaming 16-byte load (read once: no L1 allocation, evict-first in L2)
+__device__ __forceinline__ uint4 ldg_stream(const void* ptr, u64 pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ u32 sa(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n));
@@ -426,6 +437,7 @@ __device__ __forceinline__ void sched_exit(unsigned* sched, unsigned per_cta) {
 
 struct Ctx {
     int C, K, Ho, Wo, BR, BC, nt, nsm;
+    int Wi = 0;                    // input width (x)
     int act = 0;                   // activation dtype (o1d_dtype)
     std::vector<int> home;         // home table per %smid (empty: TPC-pair fallback)
     std::vector<int> table_of;
@@ -444,6 +456,17 @@ void emit_header(std::ostringstream &os, const Ctx &x) {
               "__device__ __forceinline__ float h2f(unsigned short h) { float f; asm(\"cvt.f32.f16 %0, %1;\" : \"=f\"(f) : \"h\"(h)); return f; }\n"
               "#define LD(v) h2f(v)\n"
               "__device__ __forceinline__ act_t to_act(float v) { unsigned short r; asm(\"cvt.rn.f16.f32 %0, %1;\" : \"=h\"(r) : \"f\"(v)); return r; }\n";
+    // tiles in shared memory are fp32 for every dtype: 16-bit planes are widened by the
+    // producer warps on the way in (LDG -> convert -> STS), so the tap loops never convert
+    os << "typedef float tile_t;\n#define LDT(v) (v)\n";
+    if (x.act == O1D_BF16)
+        os << "__device__ __forceinline__ float4 w4(unsigned a, unsigned b) {\n"
+              "  return make_float4(__uint_as_float(a << 16), __uint_as_float(a & 0xffff0000u), __uint_as_float(b << 16),\n"
+              "                     __uint_as_float(b & 0xffff0000u));\n}\n";
+    else if (x.act == O1D_F16)
+        os << "__device__ __forceinline__ float4 w4(unsigned a, unsigned b) {\n"
+              "  return make_float4(h2f((unsigned short)(a & 0xffffu)), h2f((unsigned short)(a >> 16)), h2f((unsigned short)(b & 0xffffu)),\n"
+              "                     h2f((unsigned short)(b >> 16)));\n}\n";
     std::vector<int> choff(x.nt + 1, 0), chlist;
     for (int t = 0; t < x.nt; ++t) {
         choff[t] = (int)chlist.size();
@@ -546,7 +569,7 @@ long emit_stencil_taps(std::ostringstream &os, const Geo &g, int pitch, const ch
     auto pname = [&](int i, int j) { return "P" + cn(i) + "_" + cn(j); };
     auto loads = [&](const Row &rw) {
         for (int j : rw.need) {
-            os << ind << "const float " << vname(rw.i, j) << " = LD(tb[" << rw.i * pitch + j << "]);\n";
+            os << ind << "const float " << vname(rw.i, j) << " = LDT(tb[" << rw.i * pitch + j << "]);\n";
             ++cost;
         }
         for (int j : rw.pr)
@@ -672,7 +695,7 @@ long emit_wgrad_pp(std::ostringstream &os, const Geo &g, const std::vector<int> 
     auto px = [&](int i, int j) {
         const std::string n = "x" + cn(i) + "_" + cn(j);
         if (loaded.insert({i, j}).second) {
-            os << ind << "const float " << n << " = LD(tb[" << i * pitch + j << "]);\n";
+            os << ind << "const float " << n << " = LDT(tb[" << i * pitch + j << "]);\n";
             ++cost;
         }
         return n;
@@ -721,7 +744,7 @@ long emit_wgrad_pp(std::ostringstream &os, const Geo &g, const std::vector<int> 
 // backward_weight of one table: rounds of <= 32 distinct offsets (register budget), each
 // folded into the per-tap sums v[k] += coef * q_d (rotation: v[k] = q_{d(k)}; duplicate taps
 // get equal sums, reading R7; bilinear taps the weighted sum of their neighbours, R14).
-long emit_wgrad_taps(std::ostringstream &os, const Geo &g, int pitch, const char *ind) {
+long emit_wgrad_taps(std::ostringstream &os, const Geo &g, int pitch, int K, const char *ind) {
     long cost = 0;
     const int nd = (int)g.taps.size();
     std::vector<int> all(nd);
@@ -729,6 +752,7 @@ long emit_wgrad_taps(std::ostringstream &os, const Geo &g, int pitch, const char
     std::stable_sort(all.begin(), all.end(), [&](int a, int b) {
         return g.taps[a].dh != g.taps[b].dh ? g.taps[a].dh < g.taps[b].dh : g.taps[a].dw < g.taps[b].dw;
     });
+    std::vector<bool> written(K, false);
     const int nr = (nd + 31) / 32;
     for (int rd = 0; rd < nr; ++rd) {
         std::vector<int> ds(all.begin() + (size_t)nd * rd / nr, all.begin() + (size_t)nd * (rd + 1) / nr);
@@ -738,12 +762,15 @@ long emit_wgrad_taps(std::ostringstream &os, const Geo &g, int pitch, const char
         cost += emit_wgrad_pp(os, g, ds, pitch, ind2.c_str());
         for (int d : ds)
             for (auto &kc : g.taps[d].ks) {
-                os << ind2 << "v[" << kc.first << "] += ";
+                os << ind2 << "v[" << kc.first << "] " << (written[kc.first] ? "+= " : "= ");
+                written[kc.first] = true;
                 if (kc.second == 1.0f) os << "q" << d << ";\n";
                 else os << flit(kc.second) << " * q" << d << ";\n";
             }
         os << ind << "}\n";
     }
+    for (int k = 0; k < K; ++k)
+        if (!written[k]) os << ind << "v[" << k << "] = 0.f;\n";
     return cost;
 }
 
@@ -766,10 +793,11 @@ bool make_lay(Lay *Lp, int pass, int wpg, const std::vector<Geo> &fwd, const std
     Lay L;
     L.wpg = wpg;
     const bool stencil = pass <= 1, wgrad = pass == 2, fused = pass == 3;
-    ring_geom(pass == 1 ? bwd : fwd, pass == 1 ? Ho : H, BR, es, &L.pitch, &L.zrows, &L.zb, &L.tb);
+    // rings hold fp32 tiles for every dtype (16-bit planes are widened by the producers)
+    ring_geom(pass == 1 ? bwd : fwd, pass == 1 ? Ho : H, BR, 4, &L.pitch, &L.zrows, &L.zb, &L.tb);
     L.hin = pass == 1 ? Ho : H;
     if (fused) {
-        ring_geom(bwd, Ho, BR, es, &L.pitch2, &L.zrows2, &L.zb2, &L.tb2);
+        ring_geom(bwd, Ho, BR, 4, &L.pitch2, &L.zrows2, &L.zb2, &L.tb2);
         L.hin2 = Ho;
     }
     if (wgrad) {
@@ -810,15 +838,16 @@ bool make_lay(Lay *Lp, int pass, int wpg, const std::vector<Geo> &fwd, const std
 
 // prologue zeroing of a ring: only what no TMA load ever writes -- the zero-row regions and
 // each slot's tail past its box
-void emit_zero_ring(std::ostringstream &os, size_t off, size_t zb, size_t tb, size_t box, int NS, int nthreads) {
+void emit_zero_ring(std::ostringstream &os, size_t off, size_t zb, size_t tb, size_t box, int NS, int nthreads,
+                    const std::string &tid = "tid") {
     const size_t tail = tb - box, stride = zb + tb;
     if (box % 16 || zb % 16 || tail % 16) {
-        os << "  for (int i = tid; i < " << (zb + NS * stride) / 16 << "; i += " << nthreads << ")\n"
+        os << "  for (int i = " << tid << "; i < " << (zb + NS * stride) / 16 << "; i += " << nthreads << ")\n"
            << "    reinterpret_cast<uint4*>(smem + " << off << ")[i] = make_uint4(0u, 0u, 0u, 0u);\n";
         return;
     }
     const size_t per = (zb + tail) / 16;
-    os << "  for (int i = tid; i < " << (NS + 1) * per << "; i += " << nthreads << ") {  // zero rows + slot tails\n"
+    os << "  for (int i = " << tid << "; i < " << (NS + 1) * per << "; i += " << nthreads << ") {  // zero rows + slot tails\n"
        << "    const int s = i / " << per << ", k = i - s * " << per << ";\n"
        << "    const int off = s * " << stride << " + (k < " << zb / 16 << " ? k * 16 : " << zb + box << " + (k - " << zb / 16
        << ") * 16);\n"
@@ -836,8 +865,8 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
        << "  float* const wsm = reinterpret_cast<float*>(smem + " << L.off_w << ");\n"
        << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
        << "  int trn = 0;\n";
-    emit_zero_ring(os, L.off_t, L.zb, L.tb, (size_t)L.hin * L.pitch * es, L.NS, nthreads);
-    if (pass == 3) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * es, L.NS, nthreads);
+    (void)nthreads;
+    (void)es;
     os << "  if (tid == 0) {\n"
        << "    for (int s = 0; s < " << L.NS << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << L.wpg << "); }\n";
     if (pass == 2) os << "    for (int q = 0; q < " << L.P << "; ++q) mbar_init(dyempty + q, " << L.wpg << ");\n";
@@ -852,9 +881,10 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
 // another pair's loads.  After the scheduler runs dry every pair gets an end marker (-1).
 void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass, int es) {
     const int NB = L.NB, P = L.P;
-    const bool wgrad = pass == 2, fused = pass == 3;
-    const size_t bytes = (size_t)L.hin * L.pitch * es + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0) +
-                         (fused ? (size_t)L.hin2 * L.pitch2 * es : 0);  // exact box bytes
+    const bool wgrad = pass == 2, fused = pass == 3, cvt = es != 4;
+    // TMA bytes the slot's full barrier expects (the widened 16-bit rings arrive by STS)
+    const size_t bytes = (cvt ? 0 : (size_t)L.hin * L.pitch * 4) + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0) +
+                         (fused && !cvt ? (size_t)L.hin2 * L.pitch2 * 4 : 0);
     const int PQ = (P + L.NPROD - 1) / L.NPROD;  // pairs per producer warp
     const int PREF = 2;                          // single-item scheduler atomics in flight
     os << "  if (warp < " << L.NPROD << ") {\n"
@@ -915,14 +945,47 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "        if (lane == 0) {\n"
        << "          s_item[s] = item;\n"
        << "          if (item >= 0) {\n"
-       << "            trace_ev(p.trace, 1, item, trn);\n"
-       << "            mbar_expect_tx(full + s, " << bytes << "u);\n"
-       << "            tma_load(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << ", &p.in_map, 0, 0, c2, n2, full + s, pol);\n";
+       << "            trace_ev(p.trace, 1, item, trn);\n";
+    if (bytes) os << "            mbar_expect_tx(full + s, " << bytes << "u);\n";
+    if (!cvt) os << "            tma_load(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << ", &p.in_map, 0, 0, c2, n2, full + s, pol);\n";
     if (wgrad) os << "            tma_load(smem + " << L.off_dy << " + q * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s, pol);\n";
-    if (fused)
+    if (fused && !cvt)
         os << "            tma_load(smem + " << L.off_t2 + L.zb2 << " + s * " << L.zb2 + L.tb2 << ", &p.aux_map, 0, 0, c2, n2, full + s, pol);\n";
     os << "          }\n"
        << "        }\n";
+    if (cvt) {
+        // 16-bit planes: every lane loads 16-byte chunks (8 elements) of the plane, all loads in
+        // flight before the first use, widens them to fp32 and stores them into the slot's
+        // image columns; the arrive below releases them to the consumers (mbarrier release)
+        auto widen = [&](const char *srcp, int Hin, int Win, size_t slot_off, size_t slot_stride, int pitch) {
+            const int cpr = Win / 8, nch = Hin * cpr, nj = (nch + 31) / 32;
+            const int ppr = (pitch - Win) / 4, npad = Hin * ppr;  // zero float4s of the pad columns
+            os << "        if (item >= 0) {\n"
+               << "          const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const act_t*>(" << srcp
+               << ") + ((u64)n2 * " << x.C << " + c2) * " << (long)Hin * Win << ");\n"
+               << "          float* dst = reinterpret_cast<float*>(smem + " << slot_off << " + s * " << slot_stride << ");\n"
+               << "          uint4 v[" << nj << "];\n"
+               << "#pragma unroll\n"
+               << "          for (int j = 0; j < " << nj << "; ++j) { const int i = lane + 32 * j; if (i < " << nch
+               << ") v[j] = ldg_stream(src + i, pol); }\n"
+               << "#pragma unroll\n"
+               << "          for (int j = 0; j < " << nj << "; ++j) {\n"
+               << "            const int i = lane + 32 * j;\n"
+               << "            if (i < " << nch << ") {\n"
+               << "              const int r = i / " << cpr << ", cc = i - r * " << cpr << ";\n"
+               << "              float4* d = reinterpret_cast<float4*>(dst + r * " << pitch << " + cc * 8);\n"
+               << "              d[0] = w4(v[j].x, v[j].y); d[1] = w4(v[j].z, v[j].w);\n"
+               << "            }\n"
+               << "          }\n"
+               << "          for (int i = lane; i < " << npad << "; i += 32) {   // columns past the image: zero (reading R1)\n"
+               << "            const int r = i / " << ppr << ", cc = i - r * " << ppr << ";\n"
+               << "            *reinterpret_cast<float4*>(dst + r * " << pitch << " + " << Win << " + cc * 4) = make_float4(0.f, 0.f, 0.f, 0.f);\n"
+               << "          }\n"
+               << "        }\n";
+        };
+        widen("p.cvt1", L.hin, pass == 1 ? x.Wo : x.Wi, L.off_t + L.zb, L.zb + L.tb, L.pitch);
+        if (fused) widen("p.cvt2", L.hin2, x.Wo, L.off_t2 + L.zb2, L.zb2 + L.tb2, L.pitch2);
+    }
     if (!wgrad)
         os << "        if (item >= 0)\n"
            << "          for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
@@ -941,7 +1004,15 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "  }\n"
        // the warps of a pair are P warp ids apart: they sit on the same SM sub-partition as
        // their producer and run the same code a few instructions apart (shared L0 I-cache)
-       << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n"
+       << "  // consumers zero what no producer ever writes (the zero rows between slots and the slot\n"
+       << "  // tails) while the producers' first loads are in flight; the regions are disjoint\n";
+    {
+        const int nc = 32 * L.ncw();
+        emit_zero_ring(os, L.off_t, L.zb, L.tb, (size_t)L.hin * L.pitch * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
+        if (fused) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
+        os << "  asm volatile(\"bar.sync 1, " << nc << ";\" ::: \"memory\");\n";
+    }
+    os << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n"
        << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n"
@@ -1035,11 +1106,11 @@ Cases stencil_cases(const std::vector<Geo> &geo, int pitch) {
     return cs;
 }
 
-Cases wgrad_cases(const std::vector<Geo> &geo, int pitch) {
+Cases wgrad_cases(const std::vector<Geo> &geo, int pitch, int K) {
     Cases cs;
     for (size_t t = 0; t < geo.size(); ++t) {
         std::ostringstream os;
-        const long c = emit_wgrad_taps(os, geo[t], pitch, "      ");
+        const long c = emit_wgrad_taps(os, geo[t], pitch, K, "      ");
         cs.body.push_back(os.str());
         cs.cost.push_back(c);
     }
@@ -1062,11 +1133,39 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
     const int nthreads = 32 * (L.ncw() + L.NPROD);
     const int NV = nv_of(x.K);
     const char *name = pass <= 1 ? "o1d_stencil" : pass == 2 ? "o1d_wgrad" : "o1d_bwd_fused";
+    if (pass == 3) {
+        // phase 1: weight-gradient partials of one item (dy block from ring 2, pixels from ring 1)
+        os << "__device__ __noinline__ void fused_wgrad(const Params& p, const tile_t* xt, const tile_t* dyt, int t, int c, int n,\n"
+           << "                                         int wg, int lane, bool active, int bc, int br) {\n"
+           << "  const tile_t* const dys = dyt + (" << R << " * br) * " << L.pitch2 << " + " << S << " * bc;\n";
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s)
+                os << "  const float g" << r << "_" << s << " = active ? LDT(dys[" << r * L.pitch2 + s << "]) : 0.f;\n";
+        os << "  float v[" << NV << "];   // v[k], k < K: assigned by the table's case\n"
+           << "#pragma unroll\n"
+           << "  for (int k = " << x.K << "; k < " << NV << "; ++k) v[k] = 0.f;\n"
+           << "  {\n";
+        emit_switch(os, wg, "xt", L.pitch, "tile_t");
+        emit_wgrad_write(os, x, L, NV);
+        os << "  }\n}\n";
+        // phase 2: backward_input band of the item from the dy tile, slot release, band store
+        os << "__device__ __noinline__ void fused_dx(const Params& p, const tile_t* dyt, const float* wv, unsigned char* stg,\n"
+           << "                                      u64* empty_s, int t, int c, int n, int row0, int lane, bool active,\n"
+           << "                                      int bc, int br) {\n";
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < S; ++s) os << "  float a" << r << "_" << s << ";\n";
+        os << "  {\n";
+        emit_switch(os, st, "dyt", L.pitch2, "tile_t");
+        os << "    __syncwarp();\n"
+           << "    if (lane == 0) mbar_arrive(empty_s);   // x + dy slot released\n";
+        emit_band_store(os, x, L);
+        os << "  }\n}\n";
+    }
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) " << name << "(const __grid_constant__ Params p) {\n";
     emit_prologue(os, L, pass, es);
     emit_producer(os, x, L, pass, es);
     os << "  // -------------------------------------------------------------- consumers\n";
-    const std::string ring1 = "reinterpret_cast<const act_t*>(smem + " + std::to_string(L.off_t + L.zb) + " + s * " +
+    const std::string ring1 = "reinterpret_cast<const tile_t*>(smem + " + std::to_string(L.off_t + L.zb) + " + s * " +
                               std::to_string(L.zb + L.tb) + ")";
     if (pass != 2) os << "  unsigned char* const stg = smem + " << L.off_stg << " + cw * " << L.sb << ";   // this warp's output band\n";
     if (pass == 2)
@@ -1077,7 +1176,7 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
         os << "    const float* wv = wsm + s * 64;\n";
         for (int r = 0; r < R; ++r)
             for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
-        emit_switch(os, st, ring1, L.pitch, "act_t");
+        emit_switch(os, st, ring1, L.pitch, "tile_t");
         os << "    __syncwarp();\n"
            << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n";
         emit_band_store(os, x, L);
@@ -1087,36 +1186,22 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
                 os << "    const float g" << r << "_" << s << " = active ? LD(dys[" << r * L.dyp + s << "]) : 0.f;\n";
         os << "    __syncwarp();\n"
            << "    if (lane == 0) mbar_arrive(dyempty + q);   // dy block in registers: the pair's dy slot is free\n"
-           << "    float v[" << NV << "];\n"
+           << "    float v[" << NV << "];   // v[k], k < K: assigned by the table's case\n"
            << "#pragma unroll\n"
-           << "    for (int k = 0; k < " << NV << "; ++k) v[k] = 0.f;\n";
-        emit_switch(os, wg, ring1, L.pitch, "act_t");
+           << "    for (int k = " << x.K << "; k < " << NV << "; ++k) v[k] = 0.f;\n";
+        emit_switch(os, wg, ring1, L.pitch, "tile_t");
         os << "    __syncwarp();\n"
            << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }  // x slot released\n";
         emit_wgrad_write(os, x, L, NV);
     } else {
         // fused backward: the weight-gradient partials (x ring 1, dy ring 2), then the
-        // backward_input band from the same dy tile; the slot is released after both
-        const std::string ring2 = "reinterpret_cast<const act_t*>(smem + " + std::to_string(L.off_t2 + L.zb2) + " + s * " +
+        // backward_input band from the same dy tile; the slot is released after both.  The two
+        // phases are separate non-inlined functions (they share no live registers; one function
+        // holding both switches took ptxas ~10x longer to compile)
+        const std::string ring2 = "reinterpret_cast<const tile_t*>(smem + " + std::to_string(L.off_t2 + L.zb2) + " + s * " +
                                   std::to_string(L.zb2 + L.tb2) + ")";
-        os << "    const float* wv = wsm + s * 64;\n"
-           << "    {\n"
-           << "      const act_t* const dys = " << ring2 << " + (" << R << " * br) * " << L.pitch2 << " + " << S << " * bc;\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s)
-                os << "      const float g" << r << "_" << s << " = active ? LD(dys[" << r * L.pitch2 + s << "]) : 0.f;\n";
-        os << "      float v[" << NV << "];\n"
-           << "#pragma unroll\n"
-           << "      for (int k = 0; k < " << NV << "; ++k) v[k] = 0.f;\n";
-        emit_switch(os, wg, ring1, L.pitch, "act_t");
-        emit_wgrad_write(os, x, L, NV);
-        os << "    }\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
-        emit_switch(os, st, ring2, L.pitch2, "act_t");
-        os << "    __syncwarp();\n"
-           << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // x + dy slot released\n";
-        emit_band_store(os, x, L);
+        os << "    fused_wgrad(p, " << ring1 << ", " << ring2 << ", t, c, n, wg, lane, active, bc, br);\n"
+           << "    fused_dx(p, " << ring2 << ", wsm + s * 64, stg, empty + s, t, c, n, row0, lane, active, bc, br);\n";
     }
     os << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
        << "  }\n";
@@ -1225,6 +1310,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
     }
     Ctx x{d.C, d.K, pl->P, pl->Q, sp->BR, sp->BC, sp->nt, nsm};
     x.act = d.dtype;
+    x.Wi = d.W;
     x.table_of.assign(pl->table_of.begin(), pl->table_of.end());
     const int P_req = env_int("O1D_P", 0), NB_req = env_int("O1D_NBUF", 0);
     const int P3_req = env_int("O1D_P3", 0);
@@ -1241,7 +1327,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
         if (!sp->has[i]) continue;
         const Lay &L = sp->lay[i];
         const Cases st = i == 2 ? Cases{} : stencil_cases(i == 0 ? sp->fwd : sp->bwd, i == 0 ? L.pitch : i == 1 ? L.pitch : L.pitch2);
-        const Cases wg = i >= 2 ? wgrad_cases(sp->fwd, L.pitch) : Cases{};
+        const Cases wg = i >= 2 ? wgrad_cases(sp->fwd, L.pitch, d.K) : Cases{};
         Ctx xi = x;
         if (gpc && !gpc->empty()) {
             // SMs per table in proportion to planes x the issue count of the table's case(s) in
@@ -1263,6 +1349,81 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
 
 }  // namespace
 
+namespace {
+const char *kSrcName[kPasses] = {"o1d_fwd.cu", "o1d_bwd_in.cu", "o1d_wgrad.cu", "o1d_bwd_fused.cu"};
+
+// compile (or take from the module cache) and load the modules of passes `which`; sets
+// launch geometry.  *all_hit: every module came from the cache.
+o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::string *src, int device, long planes,
+                       bool *all_hit) {
+    Driver &dr = drv();
+    std::vector<char> cubin[kPasses];
+    std::string logs[kPasses];
+    bool ok[kPasses] = {true, true, true, true}, need[kPasses] = {false, false, false, false};
+    *all_hit = true;
+    for (int i : which) {
+        if (i == 1 && sp->has[0] && src[1] == src[0]) continue;  // identical sources: shares pass 0's module
+        sp->mod[i] = cache_get(device, src[i]);
+        if (!sp->mod[i]) need[i] = true, *all_hit = false;
+    }
+    {
+        std::vector<std::thread> th;
+        for (int i = 0; i < kPasses; ++i)
+            if (need[i]) th.emplace_back([&, i] { ok[i] = compile_cubin(src[i], kSrcName[i], &cubin[i], &logs[i]); });
+        for (auto &t : th) t.join();
+    }
+    for (int i = 0; i < kPasses; ++i)
+        if (need[i] && !ok[i]) return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + kSrcName[i] + ":\n" + logs[i].substr(0, 4000));
+    for (int i = 0; i < kPasses; ++i) {
+        if (!need[i]) continue;
+        auto m = std::make_shared<Mod>();
+        CUresult r = dr.ctxGetCurrent(&m->ctx);
+        if (r == CUDA_SUCCESS) r = dr.moduleLoadData(&m->mod, cubin[i].data());
+        if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&m->fn, m->mod, kFnName[i]);
+        if (r == CUDA_SUCCESS && i >= 2) r = dr.moduleGetFunction(&m->fin, m->mod, "o1d_wgrad_finalize");
+        if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") + cu_err(r));
+        const std::string &lg = logs[i];
+        size_t fpos = lg.find(std::string("Compiling entry function '") + kFnName[i] + "'");
+        size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
+        m->regs = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
+        cache_put(device, src[i], m);
+        sp->mod[i] = m;
+    }
+    for (int i : which) {
+        if (i == 1 && sp->has[0] && src[1] == src[0]) sp->mod[1] = sp->mod[0];
+        const Lay &L = sp->lay[i];
+        sp->smem[i] = L.total + 16;
+        sp->threads[i] = 32 * (L.ncw() + L.NPROD);
+        CUresult r = dr.funcSetAttribute(sp->mod[i]->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)sp->smem[i]);
+        int blocks = 0;
+        if (r == CUDA_SUCCESS) r = dr.occupancy(&blocks, sp->mod[i]->fn, sp->threads[i], sp->smem[i]);
+        if (r != CUDA_SUCCESS || blocks < 1)
+            return fail(O1D_CUDA_ERROR, std::string("specialised kernel: ") + (r != CUDA_SUCCESS ? cu_err(r) : "zero occupancy"));
+        sp->grid[i] = (int)std::min<long>(planes, (long)blocks * sp->nsm);
+    }
+    return O1D_OK;
+}
+
+std::string describe_of(const o1d_plan *pl, const SpecSet *sp, bool all_hit) {
+    char buf[1200];
+    int len = snprintf(buf, sizeof buf,
+                       "spec-v2(persistent warp-specialised, 7x7 blocks, %d tap tables, %d expanded taps/channel, module cache %s",
+                       sp->nt, pl->KE, all_hit ? "hit" : "miss");
+    const char *pn[kPasses] = {"fwd", "bwd_in", "wgrad", "bwd_fused"};
+    for (int i = 0; i < kPasses && len < (int)sizeof buf; ++i) {
+        if (sp->has[i] && sp->mod[i])
+            len += snprintf(buf + len, sizeof buf - len, "; %s: %d pairs x %d warps, %d slots, grid %d, smem %zu [%s]", pn[i],
+                            sp->lay[i].P, sp->lay[i].wpg, sp->lay[i].NS, sp->grid[i], sp->smem[i], sp->mod[i]->regs.c_str());
+        else if (sp->has[i])
+            len += snprintf(buf + len, sizeof buf - len, "; %s: compiled on first use", pn[i]);
+        else
+            len += snprintf(buf + len, sizeof buf - len, "; %s: generic", pn[i]);
+    }
+    if (len < (int)sizeof buf) snprintf(buf + len, sizeof buf - len, ")%s", sp->fused_step ? " step=fused" : "");
+    return buf;
+}
+}  // namespace
+
 o1d_status spec_create(o1d_plan *pl) {
     pl->spec = nullptr;
     const o1d_desc &d = pl->d;
@@ -1276,66 +1437,28 @@ o1d_status spec_create(o1d_plan *pl) {
     std::vector<int> gpc;
     if (!gpc_map(pl->device, &gpc)) gpc.clear();
     if (!spec_prepare(pl, sp.get(), src, nsm, &gpc)) return O1D_OK;
-    const char *names[kPasses] = {"o1d_fwd.cu", "o1d_bwd_in.cu", "o1d_wgrad.cu", "o1d_bwd_fused.cu"};
     if (const char *dir = getenv("O1D_DUMP_SOURCE")) {
         for (int i = 0; i < kPasses; ++i) {
             if (!sp->has[i]) continue;
-            FILE *f = fopen((std::string(dir) + "/" + names[i]).c_str(), "w");
+            FILE *f = fopen((std::string(dir) + "/" + kSrcName[i]).c_str(), "w");
             if (f) {
                 fputs(src[i].c_str(), f);
                 fclose(f);
             }
         }
     }
-    // module cache, then NVRTC for the misses (in parallel threads)
-    std::vector<char> cubin[kPasses];
-    std::string logs[kPasses];
-    bool ok[kPasses] = {true, true, true, true}, need[kPasses] = {false, false, false, false};
+    sp->pdl = env_int("O1D_PDL", 1) != 0;
+    sp->fused_step = sp->has[3] && env_int("O1D_FUSED", 0) != 0;
+    // the fused backward is compiled on its first use unless the step uses it (its code is the
+    // backward_input and backward_weight cases together: the longest compile of the plan)
+    std::vector<int> which;
+    for (int i = 0; i < 3; ++i)
+        if (sp->has[i]) which.push_back(i);
+    if (sp->fused_step) which.push_back(3);
+    else if (sp->has[3]) sp->src3 = src[3];
     bool all_hit = true;
-    for (int i = 0; i < kPasses; ++i) {
-        if (!sp->has[i]) continue;
-        if (i == 1 && sp->has[0] && src[1] == src[0]) continue;  // identical sources: shares pass 0's module
-        sp->mod[i] = cache_get(pl->device, src[i]);
-        if (!sp->mod[i]) need[i] = true, all_hit = false;
-    }
-    {
-        std::vector<std::thread> th;
-        for (int i = 0; i < kPasses; ++i)
-            if (need[i]) th.emplace_back([&, i] { ok[i] = compile_cubin(src[i], names[i], &cubin[i], &logs[i]); });
-        for (auto &t : th) t.join();
-    }
-    for (int i = 0; i < kPasses; ++i)
-        if (need[i] && !ok[i]) return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
-    for (int i = 0; i < kPasses; ++i) {
-        if (!need[i]) continue;
-        auto m = std::make_shared<Mod>();
-        CUresult r = dr.ctxGetCurrent(&m->ctx);
-        if (r == CUDA_SUCCESS) r = dr.moduleLoadData(&m->mod, cubin[i].data());
-        if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&m->fn, m->mod, kFnName[i]);
-        if (r == CUDA_SUCCESS && i >= 2) r = dr.moduleGetFunction(&m->fin, m->mod, "o1d_wgrad_finalize");
-        if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") + cu_err(r));
-        const std::string &lg = logs[i];
-        size_t fpos = lg.find(std::string("Compiling entry function '") + kFnName[i] + "'");
-        size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
-        m->regs = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
-        cache_put(pl->device, src[i], m);
-        sp->mod[i] = m;
-    }
-    if (sp->has[1] && sp->has[0] && src[1] == src[0]) sp->mod[1] = sp->mod[0];
+    if (o1d_status st = load_passes(sp.get(), which, src, pl->device, (long)d.N * d.C, &all_hit)) return st;
     pl->jit_cache_hit = all_hit;
-    const long planes = (long)d.N * d.C;
-    for (int i = 0; i < kPasses; ++i) {
-        if (!sp->has[i]) continue;
-        const Lay &L = sp->lay[i];
-        sp->smem[i] = L.total + 16;
-        sp->threads[i] = 32 * (L.ncw() + L.NPROD);
-        CUresult r = dr.funcSetAttribute(sp->mod[i]->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)sp->smem[i]);
-        int blocks = 0;
-        if (r == CUDA_SUCCESS) r = dr.occupancy(&blocks, sp->mod[i]->fn, sp->threads[i], sp->smem[i]);
-        if (r != CUDA_SUCCESS || blocks < 1)
-            return fail(O1D_CUDA_ERROR, std::string("specialised kernel: ") + (r != CUDA_SUCCESS ? cu_err(r) : "zero occupancy"));
-        sp->grid[i] = (int)std::min<long>(planes, (long)blocks * nsm);
-    }
     const size_t nsched = (size_t)kPasses * kSlots * (sp->nt + 1) * kCS;
     if (cudaMalloc(&sp->d_sched, sizeof(unsigned) * nsched) != cudaSuccess ||
         cudaMemset(sp->d_sched, 0, sizeof(unsigned) * nsched) != cudaSuccess) {
@@ -1345,23 +1468,22 @@ o1d_status spec_create(o1d_plan *pl) {
     const char *tr = getenv("O1D_TRACE");
     if (tr && *tr && strcmp(tr, "0") != 0 && cudaMalloc(&sp->d_trace, kTraceBytes) == cudaSuccess)
         cudaMemset(sp->d_trace, 0, kTraceBytes);
-    sp->pdl = env_int("O1D_PDL", 1) != 0;
-    sp->fused_step = sp->has[3] && env_int("O1D_FUSED", 0) != 0;
-    char buf[1024];
-    int len = snprintf(buf, sizeof buf,
-                       "spec-v2(persistent warp-specialised, 7x7 blocks, %d tap tables, %d expanded taps/channel, module cache %s",
-                       sp->nt, pl->KE, all_hit ? "hit" : "miss");
-    const char *pn[kPasses] = {"fwd", "bwd_in", "wgrad", "bwd_fused"};
-    for (int i = 0; i < kPasses && len < (int)sizeof buf; ++i)
-        if (sp->has[i])
-            len += snprintf(buf + len, sizeof buf - len, "; %s: %d pairs x %d warps, %d slots, grid %d, smem %zu [%s]", pn[i],
-                            sp->lay[i].P, sp->lay[i].wpg, sp->lay[i].NS, sp->grid[i], sp->smem[i], sp->mod[i]->regs.c_str());
-        else
-            len += snprintf(buf + len, sizeof buf - len, "; %s: generic", pn[i]);
-    if (len < (int)sizeof buf) snprintf(buf + len, sizeof buf - len, ")%s", sp->fused_step ? " step=fused" : "");
-    pl->describe = buf;
-    if (getenv("O1D_VERBOSE")) fprintf(stderr, "[o1d] %s\n", buf);
+    pl->describe = describe_of(pl, sp.get(), all_hit);
+    if (getenv("O1D_VERBOSE")) fprintf(stderr, "[o1d] %s\n", pl->describe.c_str());
     pl->spec = sp.release();
+    return O1D_OK;
+}
+
+// lazy load of the fused backward (pass 3), thread-safe
+static o1d_status ensure_fused(const o1d_plan *pl) {
+    SpecSet *sp = pl->spec;
+    std::lock_guard<std::mutex> lk(sp->mu3);
+    if (sp->mod[3]) return O1D_OK;
+    std::string src[kPasses];
+    src[3] = sp->src3;
+    bool hit = true;
+    if (o1d_status st = load_passes(sp, {3}, src, pl->device, (long)pl->d.N * pl->d.C, &hit)) return st;
+    const_cast<o1d_plan *>(pl)->describe = describe_of(pl, sp, pl->jit_cache_hit);
     return O1D_OK;
 }
 
@@ -1417,11 +1539,14 @@ struct alignas(64) HostParams {
     float *dW;
     unsigned long long *trace;
     int N, n0, nlen, nowait;
+    const void *cvt1, *cvt2;
 };
 
 o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream, int n0, int nlen, bool finalize,
                     bool nowait) {
     if (nlen > 0 && !spec_window_ok(pl)) return fail(O1D_UNSUPPORTED, "batch windows need the specialised kernels");
+    if (pass == 3)
+        if (o1d_status st = ensure_fused(pl)) return st;
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
     const Lay &L = sp->lay[pass];
@@ -1430,7 +1555,13 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
     // ring-1 planes: x (passes 0, 2, 3) or dy (pass 1), box = image rows x pitch columns
     const void *in = pass == 1 ? a.dy : a.x;
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
-    if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, L.pitch, L.hin)) return st;
+    const bool cvt = d.dtype != O1D_F32;  // 16-bit rings are widened by the producers (no TMA map)
+    if (cvt) {
+        hp.cvt1 = in;
+        hp.cvt2 = a.dy;
+    } else if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, L.pitch, L.hin)) {
+        return st;
+    }
     if (pass == 0 || pass == 1 || pass == 3) {  // dense output band box for the TMA store
         void *out = pass == 0 ? a.y : a.dx;
         const int oW = pass == 0 ? pl->Q : d.W, oH = pass == 0 ? pl->P : d.H;
@@ -1439,7 +1570,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
     if (pass == 2) {  // dy plane, rows padded to whole 7-row blocks (zero-filled)
         if (o1d_status st = encode(&hp.out_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.dyp, L.dyrows)) return st;
     }
-    if (pass == 3) {  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
+    if (pass == 3 && !cvt) {  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
         if (o1d_status st = encode(&hp.aux_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.pitch2, L.hin2)) return st;
     }
     hp.w = a.w;

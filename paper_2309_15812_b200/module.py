@@ -7,8 +7,8 @@ liboriented1d.
   torch.compile / FakeTensor tracing and passes `torch.library.opcheck`.  A plan is an
   immutable host object, so the ops take an integer plan id (`register_plan`).
 * `o1d::forward` has an autograd formula: dx = backward_input(dy), dW =
-  backward_weight(x, dy) -- or, when both are needed, the fused single-pass backward
-  (o1d_backward, NEXT-2) behind one `o1d::backward` op.
+  backward_weight(x, dy) -- or, for plans created with O1D_FUSED=1, the fused
+  single-pass backward (o1d_backward, NEXT-2) behind one `o1d::backward` op.
 * `Oriented1dDWConv`: the nn.Module (C channels, K taps, D directions).
 """
 from __future__ import annotations
@@ -116,7 +116,7 @@ def _backward(ctx, dy):
     if not dy.is_contiguous():
         dy = dy.contiguous()
     need_x, need_w = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
-    if need_x and need_w:
+    if need_x and need_w and ctx.plan.fused_step:
         dx, dW = backward_op(x, dy, w, ctx.plan_id)
         return dx, dW, None
     dx = backward_input_op(dy, w, ctx.plan_id) if need_x else None
