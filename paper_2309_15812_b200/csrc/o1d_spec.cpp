@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -266,6 +267,8 @@ struct Mod {
 // launch geometry of one pass
 struct Lay {
     int P = 1, NB = 2, NS = 2, NPROD = 1, wpg = 1;
+    bool early = true;  // stencil outputs stored to the staging band row by row inside the tap code
+    int pairmap = 0;    // 0: a pair's warps on one SM sub-partition; 1: on two (pairs interleaved)
     int pitch = 0, zrows = 0, hin = 0;    // ring 1: x (passes 0, 2, 3) or dy (pass 1)
     int pitch2 = 0, zrows2 = 0, hin2 = 0; // ring 2 (fused): dy with the negated tables' halo
     int dyp = 0, dyrows = 0;              // backward_weight: dense dy box per pair
@@ -529,7 +532,12 @@ std::string merged_weight(const Tap &t) {
 // (v_j, v_j+1) register pair; a_rs = A_rs + B_rs at the end.  Footprint rows are walked
 // top to bottom, the loads of row k+1 emitted before the FMAs of row k.  Returns the
 // issue-cost estimate (FMA instructions + loads).
-long emit_stencil_taps(std::ostringstream &os, const Geo &g, int pitch, const char *ind) {
+// `store_row` (optional): called with r once output row r is final (after the last footprint row that
+// reaches it), with const float a<r>_<s> declared in scope -- the caller emits its stores there, so the
+// epilogue's shared-memory stores overlap the remaining FMAs.  Without it the outputs are assigned to
+// a<r>_<s> variables declared by the caller.
+long emit_stencil_taps(std::ostringstream &os, const Geo &g, int pitch, const char *ind,
+                       const std::function<void(int)> &store_row = nullptr) {
     long cost = 0;
     const int nd = (int)g.taps.size();
     for (int d = 0; d < nd; ++d)
@@ -578,6 +586,18 @@ long emit_stencil_taps(std::ostringstream &os, const Geo &g, int pitch, const ch
     const int nrows = (int)rows.size();
     std::map<std::string, long> last_use;
     long clock = 0;
+    int next_store = 0;
+    auto emit_final = [&](int r) {  // a_rs = A_rs + B_rs (the two column-parity sets)
+        const std::string t = store_row ? "const float a" : "a";
+        os << ind << t << r << "_0 = f2lo(A" << r << "_0) + B" << r << "_0;\n"
+           << ind << t << r << "_1 = f2hi(A" << r << "_0) + f2lo(B" << r << "_1);\n"
+           << ind << t << r << "_2 = f2lo(A" << r << "_2) + f2hi(B" << r << "_1);\n"
+           << ind << t << r << "_3 = f2hi(A" << r << "_2) + f2lo(B" << r << "_3);\n"
+           << ind << t << r << "_4 = f2lo(A" << r << "_4) + f2hi(B" << r << "_3);\n"
+           << ind << t << r << "_5 = f2hi(A" << r << "_4) + f2lo(B" << r << "_5);\n"
+           << ind << t << r << "_6 = A" << r << "_6 + f2hi(B" << r << "_5);\n";
+        if (store_row) store_row(r);
+    };
     for (int k = 0; k < nrows; ++k) {
         if (k == 0) {
             loads(rows[0]);
@@ -615,16 +635,10 @@ long emit_stencil_taps(std::ostringstream &os, const Geo &g, int pitch, const ch
                 ++cost;
             }
         emit_lru(os, ind, fm, last_use, clock);
+        if (store_row)  // output rows no later footprint row reaches are final: store them now
+            while (next_store < R && next_store + g.maxDH <= rw.i) emit_final(next_store++);
     }
-    for (int r = 0; r < R; ++r) {
-        os << ind << "a" << r << "_0 = f2lo(A" << r << "_0) + B" << r << "_0;\n"
-           << ind << "a" << r << "_1 = f2hi(A" << r << "_0) + f2lo(B" << r << "_1);\n"
-           << ind << "a" << r << "_2 = f2lo(A" << r << "_2) + f2hi(B" << r << "_1);\n"
-           << ind << "a" << r << "_3 = f2hi(A" << r << "_2) + f2lo(B" << r << "_3);\n"
-           << ind << "a" << r << "_4 = f2lo(A" << r << "_4) + f2hi(B" << r << "_3);\n"
-           << ind << "a" << r << "_5 = f2hi(A" << r << "_4) + f2lo(B" << r << "_5);\n"
-           << ind << "a" << r << "_6 = A" << r << "_6 + f2hi(B" << r << "_5);\n";
-    }
+    while (next_store < R) emit_final(next_store++);
     return cost;
 }
 
@@ -1012,7 +1026,11 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
         if (fused) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
         os << "  asm volatile(\"bar.sync 1, " << nc << ";\" ::: \"memory\");\n";
     }
-    os << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n"
+    if (L.pairmap && L.wpg == 2)  // warp wg of pair q sits next to warp 1-wg of pair q-1 (SM sub-partition = warp % 4)
+        os << "  const int cw = warp - " << L.NPROD << ", wg = cw / " << L.P << ", q = (cw - wg * " << L.P << " + wg) % " << L.P << ";\n";
+    else
+        os << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n";
+    os
        << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n"
@@ -1028,6 +1046,20 @@ void emit_loop_head(std::ostringstream &os, const Lay &L) {
        << "    if (lane == 0) trace_ev(p.trace, 3, item, trn);\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, n; item_cn(item, t, c, n, p.n0);\n";
+}
+
+// early stores (Lay::early): before the tap loop, wait until the previous band store has read the
+// staging band and point `sto` at this lane's block in it; the tap code stores each output row as
+// soon as it is final; emit_band_tail then publishes the band with one TMA store
+void emit_band_head(std::ostringstream &os, const Ctx &x, const char *ind) {
+    os << ind << "if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");  // previous band store has read stg\n"
+       << ind << "__syncwarp();\n"
+       << ind << "act_t* const sto = reinterpret_cast<act_t*>(stg) + (" << R << " * br - row0) * " << x.Wo << " + " << S << " * bc;\n";
+}
+void emit_band_tail(std::ostringstream &os, const Ctx &x, const char *ind) {
+    os << ind << "asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+       << ind << "__syncwarp();\n"
+       << ind << "if (lane == 0 && row0 < " << x.Ho << ") tma_store_band(&p.out_map, stg, row0, c, n, policy_evict_first());\n";
 }
 
 // stencil outputs: registers -> this warp's staging band -> TMA bulk store (evict-first)
@@ -1095,11 +1127,26 @@ struct Cases {
     std::vector<long> cost;
 };
 
-Cases stencil_cases(const std::vector<Geo> &geo, int pitch) {
+// stores of one final output row into this warp's staging band (`sto`, see emit_band_head)
+void emit_store_row(std::ostringstream &os, const Ctx &x, int r, const char *ind) {
+    const bool ragged = (R * x.BR != x.Ho) || (S * x.BC != x.Wo);
+    os << ind << "if (active" << (R * x.BR != x.Ho ? " && " + std::to_string(R) + " * br + " + std::to_string(r) + " < " + std::to_string(x.Ho) : "")
+       << ") {\n";
+    for (int s = 0; s < S; ++s) {
+        os << ind << "  ";
+        if (ragged && S * x.BC != x.Wo) os << "if (" << S << " * bc + " << s << " < " << x.Wo << ") ";
+        os << "sto[" << r * x.Wo + s << "] = to_act(a" << r << "_" << s << ");\n";
+    }
+    os << ind << "}\n";
+}
+
+Cases stencil_cases(const std::vector<Geo> &geo, int pitch, const Ctx *early) {
     Cases cs;
     for (size_t t = 0; t < geo.size(); ++t) {
         std::ostringstream os;
-        const long c = emit_stencil_taps(os, geo[t], pitch, "      ");
+        std::function<void(int)> st;
+        if (early) st = [&os, early](int r) { emit_store_row(os, *early, r, "      "); };
+        const long c = emit_stencil_taps(os, geo[t], pitch, "      ", st);
         cs.body.push_back(os.str());
         cs.cost.push_back(c);
     }
@@ -1152,13 +1199,16 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
         os << "__device__ __noinline__ void fused_dx(const Params& p, const tile_t* dyt, const float* wv, unsigned char* stg,\n"
            << "                                      u64* empty_s, int t, int c, int n, int row0, int lane, bool active,\n"
            << "                                      int bc, int br) {\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "  float a" << r << "_" << s << ";\n";
+        if (L.early) emit_band_head(os, x, "  ");
+        else
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) os << "  float a" << r << "_" << s << ";\n";
         os << "  {\n";
         emit_switch(os, st, "dyt", L.pitch2, "tile_t");
         os << "    __syncwarp();\n"
            << "    if (lane == 0) mbar_arrive(empty_s);   // x + dy slot released\n";
-        emit_band_store(os, x, L);
+        if (L.early) emit_band_tail(os, x, "    ");
+        else emit_band_store(os, x, L);
         os << "  }\n}\n";
     }
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) " << name << "(const __grid_constant__ Params p) {\n";
@@ -1174,12 +1224,15 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
     emit_loop_head(os, L);
     if (pass <= 1) {
         os << "    const float* wv = wsm + s * 64;\n";
-        for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
+        if (L.early) emit_band_head(os, x, "    ");
+        else
+            for (int r = 0; r < R; ++r)
+                for (int s = 0; s < S; ++s) os << "    float a" << r << "_" << s << ";\n";
         emit_switch(os, st, ring1, L.pitch, "tile_t");
         os << "    __syncwarp();\n"
            << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // done with the slot\n";
-        emit_band_store(os, x, L);
+        if (L.early) emit_band_tail(os, x, "    ");
+        else emit_band_store(os, x, L);
     } else if (pass == 2) {
         for (int r = 0; r < R; ++r)
             for (int s = 0; s < S; ++s)
@@ -1314,19 +1367,24 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
     x.table_of.assign(pl->table_of.begin(), pl->table_of.end());
     const int P_req = env_int("O1D_P", 0), NB_req = env_int("O1D_NBUF", 0);
     const int P3_req = env_int("O1D_P3", 0);
+    const bool early = env_int("O1D_EARLY", 1) != 0;
+    const int pairmap = env_int("O1D_PAIRMAP", 0);
     bool any = false;
     for (int i = 0; i < kPasses; ++i) {
         if ((i >= 2) && d.K > 32) continue;  // per-tap reduction over one warp (v[k], k < 32)
         sp->has[i] = make_lay(&sp->lay[i], i, sp->wpg, sp->fwd, sp->bwd, d.H, pl->P, pl->Q, sp->BR, sp->BC, es,
                               i == 3 ? P3_req : P_req, NB_req) &&
                      sp->lay[i].NB >= 2;
+        sp->lay[i].early = early;
+        sp->lay[i].pairmap = pairmap;
         any = any || sp->has[i];
     }
     if (!any) return false;
     for (int i = 0; i < kPasses; ++i) {
         if (!sp->has[i]) continue;
         const Lay &L = sp->lay[i];
-        const Cases st = i == 2 ? Cases{} : stencil_cases(i == 0 ? sp->fwd : sp->bwd, i == 0 ? L.pitch : i == 1 ? L.pitch : L.pitch2);
+        const Cases st = i == 2 ? Cases{} : stencil_cases(i == 0 ? sp->fwd : sp->bwd, i == 0 ? L.pitch : i == 1 ? L.pitch : L.pitch2,
+                                                          L.early ? &x : nullptr);
         const Cases wg = i >= 2 ? wgrad_cases(sp->fwd, L.pitch, d.K) : Cases{};
         Ctx xi = x;
         if (gpc && !gpc->empty()) {
