@@ -279,8 +279,26 @@ struct Lay {
     size_t ring2() const { return tb2 ? zb2 + (size_t)NS * (zb2 + tb2) : 0; }
 };
 
+// small-plane kernels (H, W <= 14): launch geometry of one pass (see gen_small_pass)
+struct SmallLay {
+    int BRs = 1, BCs = 1, QW = 1;  // 7x7 block positions per plane = warps per quad
+    int NQ = 1, NB = 2, G = 1;     // quads, input slots per quad, 32-plane groups per channel
+    int UB = 8;                    // bytes per unit (2 pixels) of the LDGSTS slots and the output staging
+    bool tma = false;              // inputs by one TMA box per item, plane-major, 4-pixel (16-byte) units
+    int UPi = 2;                   // pixels per input unit
+    int ustr = 0, lstr = 0;        // input slots: bytes between units of one plane / between planes (lanes)
+    int hp_in = 0, hp_dy = 0, hp_out = 0;  // units per plane: input, dy (backward_weight), output
+    size_t slotb = 0, dyb = 0, outb = 0;
+    size_t off_item = 0, off_w = 0, off_slot = 0, off_out = 0, total = 0;
+    int NS() const { return NQ * NB; }
+    int threads() const { return 32 * (NQ + NQ * QW); }
+};
+
 struct SpecSet {
     int BR = 0, BC = 0, wpg = 1, nt = 0, nsm = 0, K = 0;
+    bool small = false;                  // small-plane kernels (gen_small_pass) instead of gen_pass
+    long small_items = 0;                // small: work items (C x 32-plane groups)
+    SmallLay sl[3];
     bool has[kPasses] = {false, false, false, false};
     bool fused_step = false;             // o1d_step uses pass 3 (O1D_FUSED at plan creation)
     Lay lay[kPasses];
@@ -320,6 +338,9 @@ struct Params {
   int nowait;        // 1: no griddepcontrol.wait before the loads (o1d_step: inputs not from the predecessor)
   const void* cvt1;  // 16-bit plans: ring-1 planes (x or dy) widened to fp32 by the producers
   const void* cvt2;  // 16-bit fused plans: ring-2 planes (dy)
+  const void* src1;  // small-plane kernels: input planes (x, or dy for backward_input)
+  const void* src2;  // small-plane backward_weight: dy planes
+  void* dst;         // small-plane stencil: output planes (y or dx)
 };
 // streaming 16-byte load (read once: no L1 allocation, evict-first in L2)
 __device__ __forceinline__ uint4 ldg_stream(const void* ptr, u64 pol) {
@@ -1264,11 +1285,545 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
     return os.str();
 }
 
-o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH) {
+// ------------------------------------------------------------- small planes
+// Planes of at most 14 x 14 (the K-sweep's 14 x 14, ConvNeXt stage 3) do not fit the
+// warp-per-band kernels (a 7x7-block lane map covers 56 x 28 outputs) and their rows are not
+// TMA-legal (14 floats = 56 B).  Here a unit of work is 32 planes of one channel (batch samples
+// 32g .. 32g+31): lane j owns plane j, and a "quad" of BRs x BCs warps owns the item, warp bp
+// computing the 7x7 block at block position bp of all 32 planes.  The block position is a
+// compile-time constant of the warp's code, so every (output, tap) pair that falls outside the
+// image is dropped at compile time -- no zero halo in shared memory and exactly the in-bounds
+// FMAs (SURVEY 8(a1) pruning).  Shared memory holds the 32 planes unit-major: unit u (pixels
+// 2u, 2u+1 of the row-major plane) of plane j at [(u * 33 + j) * UB], so the 32 lanes reading the
+// same unit of their planes hit 32 (fp32: 16 x 8-byte) distinct banks, and a producer lane
+// copying unit u of one plane writes them with one cp.async (LDGSTS) per unit: no conversion
+// pass, no registers, completion tracked by the slot's mbarrier.
+constexpr int kSmallLanes = 33;  // unit stride in a slot: 32 planes + 1 (bank skew)
+
+// unit loads / stores of the unit-major slots (fp32: float2, 16-bit: packed u32)
+void emit_small_header(std::ostringstream &os, int act) {
+    os << "__device__ __forceinline__ void cp_async_unit(void* dst, const void* src, u64 pol) {\n";
+    if (act == O1D_F32)
+        os << "  asm volatile(\"cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\" :: \"r\"(sa(dst)), \"l\"(src), \"l\"(pol) : \"memory\");\n";
+    else
+        os << "  asm volatile(\"cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\" :: \"r\"(sa(dst)), \"l\"(src), \"l\"(pol) : \"memory\");\n";
+    os << "}\n"
+       << "__device__ __forceinline__ void cp_async_w(void* dst, const void* src) {\n"
+       << "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: \"r\"(sa(dst)), \"l\"(src) : \"memory\");\n"
+       << "}\n"
+       << "__device__ __forceinline__ void cp_async_arrive(u64* b) {\n"
+       << "  asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(sa(b)) : \"memory\");\n"
+       << "}\n";
+    if (act == O1D_F32)
+        os << "typedef float2 unit_t;\n"
+              "__device__ __forceinline__ float ulo(unit_t v) { return v.x; }\n"
+              "__device__ __forceinline__ float uhi(unit_t v) { return v.y; }\n"
+              "__device__ __forceinline__ unit_t upack(float lo, float hi) { return make_float2(lo, hi); }\n";
+    else if (act == O1D_BF16)
+        os << "typedef unsigned unit_t;\n"
+              "__device__ __forceinline__ float ulo(unit_t v) { return __uint_as_float(v << 16); }\n"
+              "__device__ __forceinline__ float uhi(unit_t v) { return __uint_as_float(v & 0xffff0000u); }\n"
+              "__device__ __forceinline__ unit_t upack(float lo, float hi) { unit_t r; asm(\"cvt.rn.bf16x2.f32 %0, %1, %2;\" : \"=r\"(r) : \"f\"(hi), \"f\"(lo)); return r; }\n";
+    else
+        os << "typedef unsigned unit_t;\n"
+              "__device__ __forceinline__ float ulo(unit_t v) { return h2f((unsigned short)(v & 0xffffu)); }\n"
+              "__device__ __forceinline__ float uhi(unit_t v) { return h2f((unsigned short)(v >> 16)); }\n"
+              "__device__ __forceinline__ unit_t upack(float lo, float hi) { unit_t r; asm(\"cvt.rn.f16x2.f32 %0, %1, %2;\" : \"=r\"(r) : \"f\"(hi), \"f\"(lo)); return r; }\n";
+}
+
+struct SmallOut {
+    int r, s, oy, ox;
+};
+
+std::vector<SmallOut> small_outs(int br, int bc, int Ho, int Wo) {
+    std::vector<SmallOut> o;
+    for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s)
+            if (R * br + r < Ho && S * bc + s < Wo) o.push_back({r, s, R * br + r, S * bc + s});
+    return o;
+}
+
+// pixel (h, w) of the unit-major input slot `base` (a per-lane pointer): loads each unit once,
+// row of units by row of units, the next row's loads ahead of the current row's FMAs.
+// `fmas[u]` = FMA statements (accumulator, text with X as the pixel placeholder) per input unit half.
+struct UnitFma {
+    std::string acc, text;  // text: statement with "@" replaced by the pixel value
+    int width = 1;          // 2: "@" is the pixel pair (i, i+1) of the unit as a packed u64
+};
+
+long emit_unit_stream(std::ostringstream &os, const std::map<int, std::vector<std::pair<int, UnitFma>>> &fm, int Win,
+                      const std::string &base, int ustr, int UP, const char *ind) {
+    long cost = 0;
+    std::vector<std::vector<int>> rows;  // units grouped by the image row of their first pixel
+    int lastrow = -1 << 30;
+    for (auto &kv : fm) {
+        const int row = (UP * kv.first) / Win;
+        if (row != lastrow) rows.push_back({}), lastrow = row;
+        rows.back().push_back(kv.first);
+    }
+    auto load = [&](const std::vector<int> &us) {
+        for (int u : us) {
+            os << ind << "const uin_t U" << u << " = *reinterpret_cast<const uin_t*>(" << base << " + " << (size_t)u * ustr
+               << ");\n";
+            ++cost;
+            std::set<int> comp;
+            for (auto &e : fm.at(u))
+                for (int w = 0; w < e.second.width; ++w) comp.insert(e.first + w);
+            for (int i : comp) os << ind << "const float P" << u << "_" << i << " = UPX(U" << u << ", " << i << ");\n";
+        }
+    };
+    std::map<std::string, long> last_use;
+    long clock = 0;
+    for (size_t k = 0; k < rows.size(); ++k) {
+        if (k == 0) {
+            load(rows[0]);
+            if (rows.size() > 1) load(rows[1]);
+        } else if (k + 1 < rows.size()) {
+            load(rows[k + 1]);
+        }
+        std::vector<std::pair<std::string, std::string>> st;
+        for (int u : rows[k])
+            for (auto &e : fm.at(u)) {
+                std::string t = e.second.text;
+                const std::string pu = "P" + std::to_string(u) + "_";
+                const std::string pv = e.second.width == 2 ? "f2pack(" + pu + std::to_string(e.first) + ", " + pu +
+                                                                 std::to_string(e.first + 1) + ")"
+                                                           : pu + std::to_string(e.first);
+                for (size_t pos; (pos = t.find('@')) != std::string::npos;) t.replace(pos, 1, pv);
+                st.push_back({e.second.acc, t});
+                ++cost;
+            }
+        emit_lru(os, ind, st, last_use, clock);
+    }
+    return cost;
+}
+
+// stencil code of one (table, block position): outputs a<r>_<s> of this lane's plane, stored
+// into the quad's output staging (`ob`, unit-major like the input slots) when complete
+long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, int Hin, int Win, int Ho, int Wo, int UB,
+                        int ustr, int UP, const char *ind) {
+    long cost = 0;
+    const int nd = (int)g.taps.size();
+    const auto outs = small_outs(br, bc, Ho, Wo);
+    std::vector<bool> used(nd, false);
+    std::map<int, std::vector<std::pair<int, UnitFma>>> fm;
+    // Packed FP32 (even Win: a pixel pair (e, e+1) with e even is an aligned register pair of its
+    // unit): the outputs (ox, ox+1) of one row take tap d with one FFMA2 when ox + dw is even and
+    // both are in the image -- accumulator pairs at even ox ("A") for even dw, at odd ox ("B") for
+    // odd dw; every other in-image (output, tap) is a scalar FMA into S_r_s.  a = A + B + S.
+    const bool packed = Win % 2 == 0;
+    std::map<std::pair<int, int>, const SmallOut *> at;  // (r, ox) -> output
+    for (auto &o : outs) at[{o.r, o.ox}] = &o;
+    auto inimg = [&](const SmallOut &o, int d) {
+        const int h = o.oy + g.taps[d].dh, w = o.ox + g.taps[d].dw;
+        return h >= 0 && h < Hin && w >= 0 && w < Win;
+    };
+    std::set<std::string> pairs_used;
+    std::set<std::pair<int, int>> scal_used;
+    for (auto &o : outs)
+        for (int d = 0; d < nd; ++d) {
+            if (!inimg(o, d)) continue;  // zero padding: dropped at compile time
+            used[d] = true;
+            const int h = o.oy + g.taps[d].dh, w = o.ox + g.taps[d].dw;
+            const int e = h * Win + w;
+            if (packed) {
+                const bool lo = (w % 2 + 2) % 2 == 0;  // this output is the low half of its pair
+                const SmallOut *mate = nullptr;
+                auto it = at.find({o.r, lo ? o.ox + 1 : o.ox - 1});
+                if (it != at.end() && inimg(*it->second, d)) mate = it->second;
+                if (mate) {
+                    if (!lo) continue;  // the pair is issued from its low half
+                    const std::string acc = std::string((o.ox % 2 == 0) ? "A" : "B") + std::to_string(o.r) + "_" + std::to_string(o.ox);
+                    pairs_used.insert(acc);
+                    UnitFma f{acc, acc + " = ffma2(@, M" + std::to_string(d) + ", " + acc + ");", 2};
+                    fm[e / UP].push_back({e % UP, f});
+                    continue;
+                }
+            }
+            scal_used.insert({o.r, o.s});
+            const std::string acc = "S" + std::to_string(o.r) + "_" + std::to_string(o.s);
+            fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = fmaf(@, m" + std::to_string(d) + ", " + acc + ");", 1}});
+        }
+    for (int d = 0; d < nd; ++d)
+        if (used[d]) {
+            os << ind << "const float m" << d << " = " << merged_weight(g.taps[d]) << ";\n";
+            if (packed) os << ind << "const u64 M" << d << " = f2pack(m" << d << ", m" << d << ");\n";
+        }
+    for (auto &a : pairs_used) os << ind << "u64 " << a << " = 0ull;\n";
+    for (auto &rs : scal_used) os << ind << "float S" << rs.first << "_" << rs.second << " = 0.f;\n";
+    cost += emit_unit_stream(os, fm, Win, "xb", ustr, UP, ind);
+    for (auto &o : outs) {  // a = A + B + S
+        std::vector<std::string> t;
+        for (const char *X : {"A", "B"}) {
+            const std::string lo = X + std::to_string(o.r) + "_" + std::to_string(o.ox);
+            const std::string hi = X + std::to_string(o.r) + "_" + std::to_string(o.ox - 1);
+            if (pairs_used.count(lo)) t.push_back("f2lo(" + lo + ")");
+            if (pairs_used.count(hi)) t.push_back("f2hi(" + hi + ")");
+        }
+        if (scal_used.count({o.r, o.s})) t.push_back("S" + std::to_string(o.r) + "_" + std::to_string(o.s));
+        os << ind << "const float a" << o.r << "_" << o.s << " = ";
+        if (t.empty()) os << "0.f";
+        for (size_t q = 0; q < t.size(); ++q) os << (q ? " + " : "") << t[q];
+        os << ";\n";
+    }
+    // outputs -> staging: pairs of one output unit held by this lane go out as one store
+    std::map<int, std::pair<std::string, std::string>> ou;  // output unit -> (lo, hi) value names
+    for (auto &o : outs) {
+        const int e = o.oy * Wo + o.ox;
+        auto &slot = ou[e >> 1];
+        (e & 1 ? slot.second : slot.first) = "a" + std::to_string(o.r) + "_" + std::to_string(o.s);
+    }
+    for (auto &kv : ou) {
+        const size_t off = (size_t)kv.first * kSmallLanes * UB;
+        const auto &lo = kv.second.first, &hi = kv.second.second;
+        if (!lo.empty() && !hi.empty()) {
+            os << ind << "*reinterpret_cast<unit_t*>(ob + " << off << ") = upack(" << lo << ", " << hi << ");\n";
+        } else {
+            const int es = UB / 2;
+            const size_t o2 = off + (lo.empty() ? es : 0);
+            os << ind << "*reinterpret_cast<act_t*>(ob + " << o2 << ") = to_act(" << (lo.empty() ? hi : lo) << ");\n";
+        }
+        ++cost;
+    }
+    return cost;
+}
+
+// backward_weight partials of one (table, block position): q_d = sum over this lane's in-image
+// (output, tap) pairs of dy * x, folded into v[k] (coefficients as emit_wgrad_taps)
+long emit_small_wgrad(std::ostringstream &os, const Geo &g, int br, int bc, int Hin, int Win, int Ho, int Wo, int K,
+                      int ustr, int UP, const char *ind) {
+    long cost = 0;
+    const int nd = (int)g.taps.size();
+    const auto outs = small_outs(br, bc, Ho, Wo);
+    // dy values of this lane's block
+    std::set<int> du;
+    for (auto &o : outs) du.insert((o.oy * Wo + o.ox) / UP);
+    for (int u : du) {
+        os << ind << "const uin_t D" << u << " = *reinterpret_cast<const uin_t*>(db + " << (size_t)u * ustr << ");\n";
+        ++cost;
+    }
+    for (auto &o : outs) {
+        const int e = o.oy * Wo + o.ox;
+        os << ind << "const float g" << o.r << "_" << o.s << " = UPX(D" << e / UP << ", " << e % UP << ");\n";
+    }
+    std::vector<bool> used(nd, false), upair(nd, false), uscal(nd, false);
+    std::map<int, std::vector<std::pair<int, UnitFma>>> fm;
+    // packed FP32 (even Win): outputs (ox, ox+1) of one row whose pixels (e, e+1) start at an even
+    // e take tap d with one FFMA2 (dy pair x pixel pair) into the pair accumulator Q<d>; the rest
+    // are scalar FMAs into q<d>
+    const bool packed = Win % 2 == 0;
+    std::map<std::pair<int, int>, const SmallOut *> at;
+    for (auto &o : outs) at[{o.r, o.ox}] = &o;
+    auto inimg = [&](const SmallOut &o, int d) {
+        const int h = o.oy + g.taps[d].dh, w = o.ox + g.taps[d].dw;
+        return h >= 0 && h < Hin && w >= 0 && w < Win;
+    };
+    auto gn = [](const SmallOut &o) { return "g" + std::to_string(o.r) + "_" + std::to_string(o.s); };
+    std::set<std::pair<int, int>> gpairs;  // (r, s): dy pair (s, s+1) packed once per item
+    for (auto &o : outs)
+        for (int d = 0; d < nd; ++d) {
+            if (!inimg(o, d)) continue;
+            used[d] = true;
+            const int h = o.oy + g.taps[d].dh, w = o.ox + g.taps[d].dw;
+            const int e = h * Win + w;
+            // (pairs only where the dy pair is aligned too: ox even, i.e. even dw -- an odd-dw pair
+            // would need its dy pair re-packed, which ptxas rematerialises at every use)
+            if (packed && Wo % 2 == 0 && ((g.taps[d].dw % 2) + 2) % 2 == 0) {
+                const bool lo = (w % 2 + 2) % 2 == 0;
+                auto it = at.find({o.r, lo ? o.ox + 1 : o.ox - 1});
+                if (it != at.end() && inimg(*it->second, d)) {
+                    if (!lo) continue;
+                    upair[d] = true;
+                    gpairs.insert({o.r, o.s});
+                    const std::string acc = "Q" + std::to_string(d);
+                    fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = ffma2(@, GP" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", " + acc + ");", 2}});
+                    continue;
+                }
+            }
+            uscal[d] = true;
+            const std::string acc = "q" + std::to_string(d);
+            fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = fmaf(" + gn(o) + ", @, " + acc + ");", 1}});
+        }
+    for (auto &rs : gpairs)
+        os << ind << "const u64 GP" << rs.first << "_" << rs.second << " = f2pack(g" << rs.first << "_" << rs.second << ", g"
+           << rs.first << "_" << rs.second + 1 << ");\n";
+    for (int d = 0; d < nd; ++d) {
+        if (upair[d]) os << ind << "u64 Q" << d << " = 0ull;\n";
+        if (uscal[d]) os << ind << "float q" << d << " = 0.f;\n";
+    }
+    cost += emit_unit_stream(os, fm, Win, "xb", ustr, UP, ind);
+    for (int d = 0; d < nd; ++d)
+        if (upair[d]) os << ind << (uscal[d] ? "q" : "const float q") << d << (uscal[d] ? " += " : " = ") << "f2lo(Q" << d
+                         << ") + f2hi(Q" << d << ");\n";
+    std::vector<bool> written(K, false);
+    for (int d = 0; d < nd; ++d) {
+        if (!used[d]) continue;
+        for (auto &kc : g.taps[d].ks) {
+            os << ind << "v[" << kc.first << "] " << (written[kc.first] ? "+= " : "= ");
+            written[kc.first] = true;
+            if (kc.second == 1.0f) os << "q" << d << ";\n";
+            else os << flit(kc.second) << " * q" << d << ";\n";
+        }
+    }
+    for (int k = 0; k < K; ++k)
+        if (!written[k]) os << ind << "v[" << k << "] = 0.f;\n";
+    return cost;
+}
+
+// layout of one small-plane pass; false if it does not fit shared memory
+bool make_small_lay(SmallLay *out, int pass, int H, int W, int Ho, int Wo, int N, int es) {
+    SmallLay L;
+    L.BRs = (Ho + R - 1) / R;
+    L.BCs = (Wo + S - 1) / S;
+    L.QW = L.BRs * L.BCs;
+    L.UB = 2 * es;
+    L.G = (N + 31) / 32;
+    const int Hin = pass == 1 ? Ho : H, Win = pass == 1 ? Wo : W;
+    // fp32 planes whose byte size is a multiple of 16 (and at most 256 elements, one TMA box row)
+    // arrive by one TMA box per item; others by per-unit cp.async (LDGSTS)
+    L.tma = es == 4 && (Hin * Win) % 4 == 0 && Hin * Win <= 256 && (pass != 2 || (Ho * Wo) % 4 == 0) && env_int("O1D_SMALL_TMA", 1);
+    L.UPi = L.tma ? 4 : 2;
+    L.ustr = L.tma ? 16 : kSmallLanes * L.UB;
+    L.lstr = L.tma ? Hin * Win * 4 : L.UB;
+    L.hp_in = Hin * Win / 2;
+    L.hp_dy = pass == 2 ? Ho * Wo / 2 : 0;
+    L.hp_out = pass <= 1 ? (pass == 0 ? Ho * Wo : H * W) / 2 : 0;
+    auto rnd = [](size_t b) { return (b + 127) & ~(size_t)127; };
+    L.slotb = rnd(L.tma ? (size_t)32 * Hin * Win * 4 : (size_t)L.hp_in * kSmallLanes * L.UB);
+    L.dyb = L.hp_dy ? rnd(L.tma ? (size_t)32 * Ho * Wo * 4 : (size_t)L.hp_dy * kSmallLanes * L.UB) : 0;
+    L.outb = L.hp_out ? rnd((size_t)L.hp_out * kSmallLanes * L.UB) : 0;
+    const size_t budget = (size_t)227 * 1024 - 64;
+    for (int NQ = std::max(1, 8 / L.QW); NQ >= 1; --NQ) {
+        for (int NB = 3; NB >= 2; --NB) {
+            if (NQ * NB > 16) continue;
+            L.NQ = NQ, L.NB = NB;
+            L.off_item = 8 * 32;  // full[16], empty[16]
+            L.off_w = L.off_item + 4 * 16;
+            L.off_slot = (L.off_w + (size_t)L.NS() * 64 * 4 + 127) & ~(size_t)127;
+            L.off_out = L.off_slot + (size_t)L.NS() * (L.slotb + L.dyb);
+            L.total = L.off_out + (size_t)NQ * L.outb;
+            // at least two quads (or 8 warps) unless a single quad is all that fits
+            if (L.total + 16 <= budget && (NB == 2 || NQ * L.QW >= 8)) {
+                *out = L;
+                return true;
+            }
+        }
+    }
+    return false;
+}
+
+void emit_finalize_ne(std::ostringstream &os, int K, const std::string &ne) {
+    os << "extern \"C\" __global__ void __launch_bounds__(256) o1d_wgrad_finalize(const float* __restrict__ ws, float* __restrict__ dW, int N) {\n"
+       << "  __shared__ double part[8][64];\n"
+       << "  pdl_wait();\n"
+       << "  pdl_trigger();\n"
+       << "  const int c = blockIdx.x, j = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+       << "  const int NE = " << ne << ";\n"
+       << "  const float* base = ws + (u64)c * NE * " << K << ";\n"
+       << "  for (int k = lane; k < " << K << "; k += 32) {\n"
+       << "    double s = 0.0;\n"
+       << "#pragma unroll 16\n"
+       << "    for (int e = j; e < NE; e += 8) s += (double)__ldcg(base + (u64)e * " << K << " + k);\n"
+       << "    part[j][k] = s;\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  for (int k = threadIdx.x; k < " << K << "; k += 256) {\n"
+       << "    double s = 0.0;\n"
+       << "    for (int q = 0; q < 8; ++q) s += part[q][k];\n"
+       << "    dW[c * " << K << " + k] = (float)s;\n"
+       << "  }\n"
+       << "}\n";
+}
+
+std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std::vector<Geo> &geo, int Hx, int Wx,
+                           std::vector<long> *cost_out) {
+    std::ostringstream os;
+    emit_header(os, x);
+    emit_small_header(os, x.act);
+    if (L.tma)
+        os << "typedef float4 uin_t;\n#define UPX(v, i) ((i) == 0 ? (v).x : (i) == 1 ? (v).y : (i) == 2 ? (v).z : (v).w)\n";
+    else
+        os << "typedef unit_t uin_t;\n#define UPX(v, i) ((i) == 0 ? ulo(v) : uhi(v))\n";
+    const int nthreads = L.threads();
+    const int NB = L.NB, QW = L.QW, NQ = L.NQ;
+    const int K = x.K;
+    const int Hin = pass == 1 ? x.Ho : Hx, Win = pass == 1 ? x.Wo : Wx;
+    const int Hout = pass == 1 ? Hx : x.Ho, Wout = pass == 1 ? Wx : x.Wo;
+    const int NV32 = (K + 31) / 32;  // backward_weight: rounds of 32 taps per warp reduction
+    // per (table, block position) case bodies
+    std::vector<std::string> body;
+    cost_out->assign(geo.size(), 0);
+    for (size_t t = 0; t < geo.size(); ++t)
+        for (int bp = 0; bp < QW; ++bp) {
+            std::ostringstream b;
+            const int br = bp / L.BCs, bc = bp % L.BCs;
+            long c = pass <= 1 ? emit_small_stencil(b, geo[t], br, bc, Hin, Win, Hout, Wout, L.UB, L.ustr, L.UPi, "      ")
+                               : emit_small_wgrad(b, geo[t], br, bc, Hin, Win, x.Ho, x.Wo, K, L.ustr, L.UPi, "      ");
+            (*cost_out)[t] += c;
+            body.push_back(b.str());
+        }
+    os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) o1d_small(const __grid_constant__ Params p) {\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
+       << "  u64* const full = reinterpret_cast<u64*>(smem);\n"
+       << "  u64* const empty = full + 16;\n"
+       << "  int* const s_item = reinterpret_cast<int*>(smem + " << L.off_item << ");\n"
+       << "  float* const wsm = reinterpret_cast<float*>(smem + " << L.off_w << ");\n"
+       << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+       << "  int trn = 0;\n"
+       << "  if (tid == 0) {\n"
+       << "    for (int s = 0; s < " << L.NS() << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << QW << "); }\n"
+       << "    fence_mbar_init();\n"
+       << "  }\n"
+       << "  __syncthreads();\n"
+       << "  const int G = (p.N + 31) / 32;   // 32-plane groups per channel\n"
+       // ------------------------------------------------------------------ producers
+       << "  if (warp < " << NQ << ") {\n"
+       << "    const int q = warp;\n"
+       << "    int tcur = 0, tried = 0;\n"
+       << "    unsigned pf0 = 0u, pf1 = 0u;\n"
+       << "    const u64 pol = policy_evict_first();\n"
+       << "    if (lane == 0) {\n"
+       << "      tcur = HOME[smid() % NHOME];\n"
+       << "      pf0 = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << "      pf1 = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << "    }\n"
+       << "    if (!p.nowait) pdl_wait();\n"
+       << "    for (int j = 0;; ++j) {\n"
+       << "      const int s = q * " << NB << " + j % " << NB << ";\n"
+       << "      if (j >= " << NB << ") mbar_wait(empty + s, ((j / " << NB << ") & 1) ^ 1);\n"
+       << "      int item = -1;\n"
+       << "      if (lane == 0) {\n"
+       << "        const unsigned v = pf0;\n"
+       << "        pf0 = pf1;\n"
+       << "        const int t0 = tcur;\n"
+       << "        item = sched_resolve(p.sched, tcur, v, tried, G);\n"
+       << "        if (tcur != t0) {\n"
+       << "          pf0 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+       << "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+       << "        } else {\n"
+       << "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+       << "        }\n"
+       << "        s_item[s] = item;\n"
+       << "      }\n"
+       << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
+       << "      if (item >= 0) {\n"
+       << "        int t, c, g; item_cn(item, t, c, g, 0);\n"
+       << "        unsigned char* const dst = smem + " << L.off_slot << " + s * " << L.slotb + L.dyb << ";\n";
+    auto copy_planes = [&](const char *src, int HW, int hp, size_t dst_off) {
+        const int nk = (hp + 31) / 32;
+        os << "        {\n"
+           << "          const unsigned char* const src = reinterpret_cast<const unsigned char*>(" << src << ") + ((u64)(32 * g) * "
+           << x.C << " + c) * " << (long)HW * (L.UB / 2) << ";\n"
+           << "#pragma unroll 1\n"
+           << "          for (int jj = 0; jj < 32; ++jj) {\n"
+           << "            if (32 * g + jj >= p.N) break;\n"
+           << "            const unsigned char* const pl = src + (u64)jj * " << (long)x.C * HW * (L.UB / 2) << ";\n"
+           << "#pragma unroll\n"
+           << "            for (int k = 0; k < " << nk << "; ++k) {\n"
+           << "              const int u = lane + 32 * k;\n"
+           << "              if (u < " << hp << ") cp_async_unit(dst + " << dst_off << " + (u * " << kSmallLanes << " + jj) * " << L.UB
+           << ", pl + u * " << L.UB << ", pol);\n"
+           << "            }\n"
+           << "          }\n"
+           << "        }\n";
+    };
+    if (L.tma) {  // one box (all pixels, this channel, 32 samples; samples past the batch zero-filled)
+        os << "        if (lane == 0) {\n"
+           << "          mbar_expect_tx(full + s, " << L.slotb + L.dyb << "u);\n"
+           << "          tma_load(dst, &p.in_map, 0, 0, c, 32 * g, full + s, pol);\n";
+        if (pass == 2) os << "          tma_load(dst + " << L.slotb << ", &p.aux_map, 0, 0, c, 32 * g, full + s, pol);\n";
+        os << "        }\n";
+    } else {
+        copy_planes("p.src1", Hin * Win, L.hp_in, 0);
+        if (pass == 2) copy_planes("p.src2", x.Ho * x.Wo, L.hp_dy, L.slotb);
+    }
+    if (pass <= 1)
+        os << "        for (int k = lane; k < " << K << "; k += 32) cp_async_w(wsm + s * 64 + k, p.w + c * " << K << " + k);\n";
+    os << "      }\n"
+       << "      cp_async_arrive(full + s);   // 32 lanes: each arrival fires when the lane's copies have landed\n"
+       << "      if (item < 0) break;\n"
+       << "    }\n"
+       << "    if (p.nowait) pdl_wait();\n"
+       << "    pdl_trigger();\n"
+       << "    if (lane == 0) sched_exit(p.sched, " << NQ << "u);\n"
+       << "    return;\n"
+       << "  }\n"
+       // ------------------------------------------------------------------ consumers
+       << "  const int cw = warp - " << NQ << ", q = cw / " << QW << ", bp = cw % " << QW << ";\n";
+    if (pass <= 1)
+        os << "  unsigned char* const ob = smem + " << L.off_out << " + q * " << L.outb << " + lane * " << L.UB << ";\n";
+    os << "  for (int it = 0;; ++it) {\n"
+       << "    const int s = q * " << NB << " + it % " << NB << ";\n"
+       << "    mbar_wait(full + s, (it / " << NB << ") & 1);\n"
+       << "    const int item = s_item[s];\n"
+       << "    if (item < 0) break;\n"
+       << "    int t, c, g; item_cn(item, t, c, g, 0);\n"
+       << "    const unsigned char* const xb = smem + " << L.off_slot << " + s * " << L.slotb + L.dyb << " + lane * " << L.lstr << ";\n";
+    if (pass <= 1) {
+        os << "    const float* const wv = wsm + s * 64;\n"
+           << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * QW << ") : \"memory\");   // previous write-back done\n"
+           << "    switch (t * " << QW << " + bp) {\n";
+        for (size_t i = 0; i < body.size(); ++i) os << "    case " << i << ": {\n" << body[i] << "      break;\n    }\n";
+        os << "    }\n"
+           << "    __syncwarp();\n"
+           << "    if (lane == 0) mbar_arrive(empty + s);   // input slot free\n"
+           << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * QW << ") : \"memory\");   // all blocks staged\n"
+           // write-back: warp bp stores planes bp, bp + QW, ... (coalesced along each plane)
+           << "    {\n"
+           << "      const int HWo = " << Hout * Wout << ";\n"
+           << "      unsigned char* const dbase = reinterpret_cast<unsigned char*>(p.dst) + ((u64)(32 * g) * " << x.C
+           << " + c) * (u64)HWo * " << L.UB / 2 << ";\n"
+           << "      const unsigned char* const obq = smem + " << L.off_out << " + q * " << L.outb << ";\n"
+           << "#pragma unroll 1\n"
+           << "      for (int jj = bp; jj < 32; jj += " << QW << ") {\n"
+           << "        if (32 * g + jj >= p.N) break;\n"
+           << "        unsigned char* const pl = dbase + (u64)jj * " << (long)x.C * Hout * Wout * (L.UB / 2) << ";\n"
+           << "#pragma unroll\n"
+           << "        for (int k = 0; k < " << (L.hp_out + 31) / 32 << "; ++k) {\n"
+           << "          const int u = lane + 32 * k;\n"
+           << "          if (u < " << L.hp_out << ") {\n"
+           << "            const unit_t v = *reinterpret_cast<const unit_t*>(obq + (u * " << kSmallLanes << " + jj) * " << L.UB << ");\n"
+           << "            __stcs(reinterpret_cast<unit_t*>(pl) + u, v);\n"
+           << "          }\n"
+           << "        }\n"
+           << "      }\n"
+           << "    }\n";
+    } else {
+        os << "    const unsigned char* const db = xb + " << L.slotb << ";\n"
+           << "    float v[" << 32 * NV32 << "];\n"
+           << "#pragma unroll\n"
+           << "    for (int k = " << K << "; k < " << 32 * NV32 << "; ++k) v[k] = 0.f;\n"
+           << "    switch (t * " << QW << " + bp) {\n";
+        for (size_t i = 0; i < body.size(); ++i) os << "    case " << i << ": {\n" << body[i] << "      break;\n    }\n";
+        os << "    }\n"
+           << "    __syncwarp();\n"
+           << "    if (lane == 0) mbar_arrive(empty + s);   // input slot free\n"
+           << "    if (32 * g + lane >= p.N) {   // lanes past the batch hold stale planes\n"
+           << "#pragma unroll\n"
+           << "      for (int k = 0; k < " << 32 * NV32 << "; ++k) v[k] = 0.f;\n"
+           << "    }\n";
+        for (int rd = 0; rd < NV32; ++rd) {
+            os << "    {\n"
+               << "      float vv[32];\n"
+               << "#pragma unroll\n"
+               << "      for (int k = 0; k < 32; ++k) vv[k] = v[" << 32 * rd << " + k];\n"
+               << "      const float part = reduce_scatter<32>(vv, lane);\n"
+               << "      if (" << 32 * rd << " + lane < " << K << ") p.ws[(((u64)c * G + g) * " << QW << " + bp) * " << K << " + "
+               << 32 * rd << " + lane] = part;\n"
+               << "    }\n";
+        }
+    }
+    os << "  }\n"
+       << "}\n";
+    if (pass == 2) emit_finalize_ne(os, K, "((N + 31) / 32) * " + std::to_string(QW));
+    return os.str();
+}
+
+o1d_status encode(CUtensorMap *m, const void *ptr, int dtype, int W, int H, int C, int N, int boxW, int boxH, int boxN = 1) {
     const size_t es = dtype_size(dtype);
     cuuint64_t dims[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)C, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)W * es, (cuuint64_t)W * H * es, (cuuint64_t)W * H * C * es};
-    cuuint32_t box[4] = {(cuuint32_t)boxW, (cuuint32_t)boxH, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)boxW, (cuuint32_t)boxH, 1, (cuuint32_t)boxN};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUtensorMapDataType dt = dtype == O1D_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : dtype == O1D_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -1331,13 +1886,58 @@ void cache_put(int dev, const std::string &src, const std::shared_ptr<Mod> &m) {
 
 const char *kFnName[kPasses] = {"o1d_stencil", "o1d_stencil", "o1d_wgrad", "o1d_bwd_fused"};
 
+// small planes (H, W <= 14): passes 0-2 on gen_small_pass, no fused backward
+bool small_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int nsm, const std::vector<int> *gpc) {
+    const o1d_desc &d = pl->d;
+    const int es = (int)dtype_size(d.dtype);
+    sp->small = true;
+    sp->small_items = (long)d.C * ((d.N + 31) / 32);
+    sp->nt = pl->n_distinct;
+    sp->nsm = nsm;
+    sp->K = d.K;
+    std::vector<int> rep(sp->nt, -1);
+    std::vector<long> count(sp->nt, 0);
+    for (int c = 0; c < d.C; ++c) {
+        if (rep[pl->table_of[c]] < 0) rep[pl->table_of[c]] = c;
+        count[pl->table_of[c]] += 1;
+    }
+    for (int t = 0; t < sp->nt; ++t) {
+        const size_t o = (size_t)rep[t] * pl->KE;
+        sp->fwd.push_back(make_geo(&pl->eoh[o], &pl->eow[o], &pl->ek[o], &pl->ecoef[o], pl->KE, false, 1, d.W));
+        sp->bwd.push_back(make_geo(&pl->eoh[o], &pl->eow[o], &pl->ek[o], &pl->ecoef[o], pl->KE, true, 1, pl->Q));
+    }
+    Ctx x{d.C, d.K, pl->P, pl->Q, 1, 1, sp->nt, nsm};
+    x.act = d.dtype;
+    x.Wi = d.W;
+    x.table_of.assign(pl->table_of.begin(), pl->table_of.end());
+    for (int i = 0; i < 3; ++i) {
+        sp->has[i] = make_small_lay(&sp->sl[i], i, d.H, d.W, pl->P, pl->Q, d.N, es);
+        if (!sp->has[i]) continue;
+        std::vector<long> cost;
+        Ctx xi = x;
+        // the case costs are only known after generation: generate once for the costs, then
+        // again with the SM placement they imply (the source text differs only in HOME)
+        src[i] = gen_small_pass(xi, sp->sl[i], i, i == 1 ? sp->bwd : sp->fwd, d.H, d.W, &cost);
+        if (gpc && !gpc->empty()) {
+            std::vector<long> work(sp->nt);
+            for (int t = 0; t < sp->nt; ++t) work[t] = count[t] * (100 + cost[t]);
+            xi.home = home_tables(*gpc, work, sp->nt);
+            src[i] = gen_small_pass(xi, sp->sl[i], i, i == 1 ? sp->bwd : sp->fwd, d.H, d.W, &cost);
+        }
+    }
+    return sp->has[0] || sp->has[1] || sp->has[2];
+}
+
 // Host-only part: eligibility, geometry and generated sources (no CUDA calls).
 // Returns false (and no sources) when the plan is not eligible for any pass.
 bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int nsm, const std::vector<int> *gpc) {
     const o1d_desc &d = pl->d;
     const int es = (int)dtype_size(d.dtype);
     if (d.stride != 1) return false;  // stride 2 runs on the generic kernels
-    if ((d.W * es) % 16 != 0 || d.K > 64) return false;
+    if (d.K > 64 || pl->n_distinct > 16) return false;
+    if (d.H <= 2 * R && d.W <= 2 * S && (d.H * d.W) % 2 == 0 && env_int("O1D_SMALL", 1) != 0)
+        return small_prepare(pl, sp, src, nsm, gpc);
+    if ((d.W * es) % 16 != 0) return false;
     if (pl->n_distinct > 16 || (long)d.N * d.C >= (1L << 22)) return false;
     if (d.W > 256 || d.H > 256) return false;
     sp->BR = (pl->P + R - 1) / R;
@@ -1437,11 +2037,11 @@ o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::st
         auto m = std::make_shared<Mod>();
         CUresult r = dr.ctxGetCurrent(&m->ctx);
         if (r == CUDA_SUCCESS) r = dr.moduleLoadData(&m->mod, cubin[i].data());
-        if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&m->fn, m->mod, kFnName[i]);
+        if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&m->fn, m->mod, sp->small ? "o1d_small" : kFnName[i]);
         if (r == CUDA_SUCCESS && i >= 2) r = dr.moduleGetFunction(&m->fin, m->mod, "o1d_wgrad_finalize");
         if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") + cu_err(r));
         const std::string &lg = logs[i];
-        size_t fpos = lg.find(std::string("Compiling entry function '") + kFnName[i] + "'");
+        size_t fpos = lg.find(std::string("Compiling entry function '") + (sp->small ? "o1d_small" : kFnName[i]) + "'");
         size_t pos = lg.find("Used ", fpos == std::string::npos ? 0 : fpos);
         m->regs = pos == std::string::npos ? "?" : lg.substr(pos, lg.find('\n', pos) - pos);
         cache_put(device, src[i], m);
@@ -1449,21 +2049,42 @@ o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::st
     }
     for (int i : which) {
         if (i == 1 && sp->has[0] && src[1] == src[0]) sp->mod[1] = sp->mod[0];
-        const Lay &L = sp->lay[i];
-        sp->smem[i] = L.total + 16;
-        sp->threads[i] = 32 * (L.ncw() + L.NPROD);
+        if (sp->small) {
+            sp->smem[i] = sp->sl[i].total + 16;
+            sp->threads[i] = sp->sl[i].threads();
+        } else {
+            const Lay &L = sp->lay[i];
+            sp->smem[i] = L.total + 16;
+            sp->threads[i] = 32 * (L.ncw() + L.NPROD);
+        }
         CUresult r = dr.funcSetAttribute(sp->mod[i]->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)sp->smem[i]);
         int blocks = 0;
         if (r == CUDA_SUCCESS) r = dr.occupancy(&blocks, sp->mod[i]->fn, sp->threads[i], sp->smem[i]);
         if (r != CUDA_SUCCESS || blocks < 1)
             return fail(O1D_CUDA_ERROR, std::string("specialised kernel: ") + (r != CUDA_SUCCESS ? cu_err(r) : "zero occupancy"));
-        sp->grid[i] = (int)std::min<long>(planes, (long)blocks * sp->nsm);
+        sp->grid[i] = (int)std::min<long>(sp->small ? sp->small_items : planes, (long)blocks * sp->nsm);
     }
     return O1D_OK;
 }
 
 std::string describe_of(const o1d_plan *pl, const SpecSet *sp, bool all_hit) {
     char buf[1200];
+    if (sp->small) {
+        int len = snprintf(buf, sizeof buf,
+                           "spec-small(32-plane items, 7x7 blocks at compile-time positions, %d tap tables, module cache %s",
+                           sp->nt, all_hit ? "hit" : "miss");
+        const char *pn[3] = {"fwd", "bwd_in", "wgrad"};
+        for (int i = 0; i < 3 && len < (int)sizeof buf; ++i) {
+            const SmallLay &L = sp->sl[i];
+            if (sp->has[i] && sp->mod[i])
+                len += snprintf(buf + len, sizeof buf - len, "; %s: %d quads x %d warps, %d slots, grid %d, smem %zu [%s]", pn[i],
+                                L.NQ, L.QW, L.NS(), sp->grid[i], sp->smem[i], sp->mod[i]->regs.c_str());
+            else
+                len += snprintf(buf + len, sizeof buf - len, "; %s: generic", pn[i]);
+        }
+        if (len < (int)sizeof buf) snprintf(buf + len, sizeof buf - len, "; bwd_fused: generic)");
+        return buf;
+    }
     int len = snprintf(buf, sizeof buf,
                        "spec-v2(persistent warp-specialised, 7x7 blocks, %d tap tables, %d expanded taps/channel, module cache %s",
                        sp->nt, pl->KE, all_hit ? "hit" : "miss");
@@ -1559,7 +2180,7 @@ bool spec_step_fused(const o1d_plan *pl) { return pl->spec && pl->spec->fused_st
 // batch windows (o1d_step_host pipelining): every pass of the step on the specialised kernels
 bool spec_window_ok(const o1d_plan *pl) {
     const SpecSet *sp = pl->spec;
-    return sp && sp->has[0] && ((sp->has[1] && sp->has[2]) || sp->fused_step);
+    return sp && !sp->small && sp->has[0] && ((sp->has[1] && sp->has[2]) || sp->fused_step);
 }
 o1d_status spec_finalize(const o1d_plan *pl, int pass, float *dW, const float *ws, void *stream) {
     const SpecSet *sp = pl->spec;
@@ -1584,6 +2205,7 @@ o1d_status spec_finalize(const o1d_plan *pl, int pass, float *dW, const float *w
 int spec_launches(const o1d_plan *, int pass) { return pass >= 2 ? 2 : 1; }
 size_t spec_workspace_bytes(const o1d_plan *pl) {
     if (!pl->spec) return 0;
+    if (pl->spec->small) return sizeof(float) * (size_t)pl->d.C * pl->spec->sl[2].G * pl->spec->sl[2].QW * pl->d.K;
     return sizeof(float) * (size_t)pl->d.N * pl->d.C * pl->spec->wpg * pl->d.K;
 }
 
@@ -1598,6 +2220,8 @@ struct alignas(64) HostParams {
     unsigned long long *trace;
     int N, n0, nlen, nowait;
     const void *cvt1, *cvt2;
+    const void *src1, *src2;
+    void *dst;
 };
 
 o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream, int n0, int nlen, bool finalize,
@@ -1610,6 +2234,18 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
     const Lay &L = sp->lay[pass];
     HostParams hp;
     std::memset(&hp, 0, sizeof hp);
+    if (sp->small) {
+        hp.src1 = pass == 1 ? a.dy : a.x;
+        hp.src2 = a.dy;
+        hp.dst = pass == 0 ? a.y : a.dx;
+        if (sp->sl[pass].tma) {  // planes as rows of H*W elements: one box = 32 samples of one channel
+            const int hwi = pass == 1 ? pl->P * pl->Q : d.H * d.W;
+            if (o1d_status st = encode(&hp.in_map, hp.src1, d.dtype, hwi, 1, d.C, d.N, hwi, 1, 32)) return st;
+            if (pass == 2)
+                if (o1d_status st = encode(&hp.aux_map, a.dy, d.dtype, pl->P * pl->Q, 1, d.C, d.N, pl->P * pl->Q, 1, 32))
+                    return st;
+        }
+    } else {
     // ring-1 planes: x (passes 0, 2, 3) or dy (pass 1), box = image rows x pitch columns
     const void *in = pass == 1 ? a.dy : a.x;
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
@@ -1630,6 +2266,7 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
     }
     if (pass == 3 && !cvt) {  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
         if (o1d_status st = encode(&hp.aux_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.pitch2, L.hin2)) return st;
+    }
     }
     hp.w = a.w;
     hp.ws = a.ws;

@@ -142,8 +142,10 @@ def test_spec_source_compiles_for_sm100a(tmp_path, pass_id, disc):
 
 def test_spec_source_ineligible_shapes():
     with pytest.raises(B.O1DError) as e:
-        B.spec_source(1, 8, 14, 14, 7, np.zeros(8), 0)  # 14*4 B rows are not TMA-legal
+        B.spec_source(1, 8, 30, 30, 7, np.zeros(8), 0)  # 30*4 B rows: not TMA-legal, too big for small planes
     assert e.value.status == 5
+    with pytest.raises(B.O1DError):
+        B.spec_source(1, 8, 7, 7, 7, np.zeros(8), 0)  # odd H*W: no 2-pixel units
     with pytest.raises(B.O1DError):
         B.spec_source(1, 8, 56, 56, 7, np.zeros(8), 0, stride=2)
 
@@ -167,3 +169,25 @@ def test_make_taps_shear_bit_exact():
     a = np.zeros(2)
     o1, o2 = np.empty((2, 7), np.int16), np.empty((2, 7), np.int16)
     assert B.lib().o1d_make_taps_ex(7, 3, 2, a.ctypes.data, 5, o1.ctypes.data, o2.ctypes.data) == 1  # INVALID_ARG
+
+
+@pytest.mark.parametrize("dtype,pass_id", [("f32", 0), ("f32", 2), ("bf16", 1)])
+def test_small_plane_source_compiles_for_sm100a(tmp_path, pass_id, dtype):
+    """Planes of at most 14 x 14 get the small-plane kernels (32-plane items, compile-time block
+    positions, exact pruning of out-of-image taps): valid sm_100a code, TMA box loads for fp32
+    planes of 16-byte multiples, cp.async (LDGSTS) units otherwise, packed FP32 in the tap code."""
+    import shutil
+    import subprocess
+    import torch
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    src = B.spec_source(128, 16, 14, 14, 31, T.direction_angles(4, 16, "cycled"), pass_id, dtype=dt)
+    assert "o1d_small" in src
+    f = tmp_path / f"s{pass_id}.cu"
+    f.write_text(src)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-o", str(tmp_path / "s.cubin"),
+                        str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    sass = subprocess.run(["cuobjdump", "-sass", str(tmp_path / "s.cubin")], capture_output=True, text=True).stdout
+    assert "FFMA2" in sass
+    assert ("UTMALDG" in sass) == (dtype == "f32") and ("LDGSTS.E" in sass) == (dtype != "f32" or pass_id <= 1)

@@ -56,6 +56,8 @@ def run_case(N, C, H, W, K, angles, stride=1, dtype=torch.float32, flags=0, thre
                   discretization=disc)
     if expect == "spec":
         assert plan.describe().startswith("spec"), plan.describe()
+    elif expect == "spec-small":
+        assert plan.describe().startswith("spec-small"), plan.describe()
     elif expect == "generic":
         assert plan.describe().startswith("generic"), plan.describe()
     P, Q = plan.P, plan.Q
@@ -491,3 +493,29 @@ def test_torch_library_opcheck():
     y.backward(dy)
     assert torch.equal(x.grad, B.backward_input(plan, dy, w.detach()))
     assert torch.equal(w.grad, B.backward_weight(plan, x.detach(), dy))
+
+
+# small-plane kernels (H, W <= 14, even H*W): 32-plane items, compile-time block positions with
+# the out-of-image (output, tap) pairs dropped; partial last groups (N not a multiple of 32),
+# ragged blocks, K up to 63 (taps that never reach the image), both activation widths
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("HW,N,K,assign", [((14, 14), 33, 31, "cycled"), ((14, 14), 70, 63, "contiguous"),
+                                           ((12, 14), 5, 15, "cycled"), ((8, 8), 40, 7, "contiguous"),
+                                           ((6, 4), 3, 31, "cycled"), ((14, 10), 32, 27, "cycled"),
+                                           ((2, 2), 2, 7, "cycled"), ((7, 14), 9, 31, "contiguous")])
+def test_small_planes(dtype, HW, N, K, assign):
+    C = 16
+    angles = B.direction_angles(8, C, assign)
+    run_case(N, C, HW[0], HW[1], K, angles, dtype=dtype, check_det=True, expect="spec-small")
+
+
+@pytest.mark.parametrize("angle_set", sorted(SPEC_SETS))
+def test_small_planes_angle_sets(angle_set):
+    angles = SPEC_SETS[angle_set]
+    run_case(3, len(angles), 14, 14, 31, angles, expect="spec-small")
+
+
+@pytest.mark.parametrize("disc", ["shear", "bilinear"])
+def test_small_planes_discretizations(disc):
+    angles = B.direction_angles(8, 16, "cycled")
+    run_case(35, 16, 14, 14, 31, angles, disc=disc, expect="spec-small")
