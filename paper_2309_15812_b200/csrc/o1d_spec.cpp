@@ -274,6 +274,10 @@ struct Lay {
     int dyp = 0, dyrows = 0;              // backward_weight: dense dy box per pair
     size_t zb = 0, tb = 0, zb2 = 0, tb2 = 0, db = 0, sb = 0;
     size_t off_item = 0, off_w = 0, off_stg = 0, off_dy = 0, off_t = 0, off_t2 = 0, total = 0;
+    // 16-bit ring-1 planes: staged = one TMA box of the raw plane into a per-pair staging buffer,
+    // widened to the fp32 slot by the pair's producer (else: per-lane 16-byte loads, see emit_producer)
+    bool staged = false;
+    size_t stb = 0, off_st = 0;
     int ncw() const { return P * wpg; }
     size_t ring1() const { return zb + (size_t)NS * (zb + tb); }
     size_t ring2() const { return tb2 ? zb2 + (size_t)NS * (zb2 + tb2) : 0; }
@@ -843,28 +847,37 @@ bool make_lay(Lay *Lp, int pass, int wpg, const std::vector<Geo> &fwd, const std
     }
     const size_t budget = (size_t)227 * 1024 - 64;
     const int NSmax = 16;
+    // staged 16-bit loads for the stencil passes (measured: forward 50.8 -> 49.1 us at S1 bf16; the
+    // weight gradient was slower staged, 52.4 -> 55.0 us, and keeps the per-lane loads)
+    bool stage = es != 4 && stencil && env_int("O1D_STAGE", 1) != 0;
     auto fit = [&](int P, int NB) {
         L.P = P, L.NB = NB, L.NS = P * NB;
         if (L.NS > NSmax || P * wpg > 15) return false;
         L.NPROD = P <= 4 ? P : 2;
         // header: full[16], empty[16], dyempty[8] mbarriers | s_item[16] | weights | bands | dy slots | rings
-        L.off_item = 8 * (2 * (size_t)NSmax + 8);
+        L.off_item = 8 * (2 * (size_t)NSmax + 16);  // + stfull[8]
         L.off_w = (L.off_item + 4 * (size_t)NSmax + 15) & ~(size_t)15;
         L.off_stg = (L.off_w + (wgrad ? 0 : (size_t)L.NS * 64 * 4) + 127) & ~(size_t)127;
         L.sb = (stencil || fused) ? (((size_t)4 * R * Wo * es + 127) & ~(size_t)127) : 0;
         L.off_dy = L.off_stg + (size_t)L.ncw() * L.sb;
         L.off_t = (L.off_dy + (size_t)P * L.db + 1023) & ~(size_t)1023;
         L.off_t2 = L.off_t + L.ring1();
-        L.total = L.off_t2 + L.ring2();
+        L.off_st = L.off_t2 + L.ring2();
+        L.staged = stage && P <= 4;
+        L.stb = L.staged ? (((size_t)L.hin * Wo * es + 127) & ~(size_t)127) : 0;
+        L.total = L.off_st + (size_t)P * L.stb;
         return L.total + 16 <= budget;
     };
     bool ok = false;
-    if (P_req > 0) {
-        ok = fit(P_req, std::max(1, NB_req > 0 ? NB_req : 2));
-    } else {
-        // default: 8 consumer warps (4 pairs at 56x56), two slots per pair; fewer pairs when the
-        // slots do not fit (the fused kernel's x + dy slots)
-        for (int P = std::max(1, std::min(8, 8 / wpg)); P >= 1 && !ok; --P) ok = fit(P, NB_req > 0 ? NB_req : 2);
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt, stage = false) {
+        if (P_req > 0) {
+            ok = fit(P_req, std::max(1, NB_req > 0 ? NB_req : 2));
+        } else {
+            // default: 8 consumer warps (4 pairs at 56x56), two slots per pair; fewer pairs when the
+            // slots do not fit (the fused kernel's x + dy slots)
+            for (int P = std::max(1, std::min(8, 8 / wpg)); P >= 1 && !ok; --P) ok = fit(P, NB_req > 0 ? NB_req : 2);
+        }
+        if (ok && stage && L.P < 4 && es != 4) ok = false;  // staging must not cost consumer pairs: retry without
     }
     if (!ok) return false;
     *Lp = L;
@@ -905,6 +918,7 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
     os << "  if (tid == 0) {\n"
        << "    for (int s = 0; s < " << L.NS << "; ++s) { mbar_init(full + s, 32); mbar_init(empty + s, " << L.wpg << "); }\n";
     if (pass == 2) os << "    for (int q = 0; q < " << L.P << "; ++q) mbar_init(dyempty + q, " << L.wpg << ");\n";
+    if (L.staged) os << "    for (int q = 0; q < " << L.P << "; ++q) mbar_init(full + 40 + q, 1);   // stfull: raw plane staged\n";
     os << "    fence_mbar_init();\n"
        << "  }\n"
        << "  __syncthreads();\n";
@@ -914,7 +928,13 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
 // q*NB + j % NB.  One producer per pair (P <= 4) sleeps in try_wait until the pair frees a
 // slot; with more pairs two producers poll theirs round-robin so a slow pair never holds up
 // another pair's loads.  After the scheduler runs dry every pair gets an end marker (-1).
+void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, int pass, int es);
+
 void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass, int es) {
+    if (L.staged) {
+        emit_producer_staged(os, x, L, pass, es);
+        return;
+    }
     const int NB = L.NB, P = L.P;
     const bool wgrad = pass == 2, fused = pass == 3, cvt = es != 4;
     // TMA bytes the slot's full barrier expects (the widened 16-bit rings arrive by STS)
@@ -1036,14 +1056,28 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "    pdl_trigger();\n"
        << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
        << "    return;\n"
-       << "  }\n"
-       // the warps of a pair are P warp ids apart: they sit on the same SM sub-partition as
-       // their producer and run the same code a few instructions apart (shared L0 I-cache)
-       << "  // consumers zero what no producer ever writes (the zero rows between slots and the slot\n"
+       << "  }\n";
+}
+
+// consumer set-up after the producer branch: zeroing of what no producer writes, then the warp's
+// pair / band / lane block
+void emit_consumer_prologue(std::ostringstream &os, const Ctx &x, const Lay &L, int pass) {
+    const bool fused = pass == 3;
+    // the warps of a pair are P warp ids apart: they sit on the same SM sub-partition as
+    // their producer and run the same code a few instructions apart (shared L0 I-cache)
+    os << "  // consumers zero what no producer ever writes (the zero rows between slots and the slot\n"
        << "  // tails) while the producers' first loads are in flight; the regions are disjoint\n";
     {
         const int nc = 32 * L.ncw();
         emit_zero_ring(os, L.off_t, L.zb, L.tb, (size_t)L.hin * L.pitch * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
+        if (L.staged) {  // columns [W, pitch) of every slot row: the widening producers write only [0, W)
+            const int ppr = (L.pitch - x.Wo) / 4;
+            os << "  for (int i = tid - " << 32 * L.NPROD << "; i < " << L.NS * L.hin * ppr << "; i += " << nc << ") {\n"
+               << "    const int s = i / " << L.hin * ppr << ", k = i - s * " << L.hin * ppr << ", r = k / " << ppr << ", cc = k - r * " << ppr << ";\n"
+               << "    *reinterpret_cast<float4*>(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << " + (r * " << L.pitch << " + "
+               << x.Wo << " + cc * 4) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);\n"
+               << "  }\n";
+        }
         if (fused) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
         os << "  asm volatile(\"bar.sync 1, " << nc << ";\" ::: \"memory\");\n";
     }
@@ -1056,6 +1090,113 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n"
        << "  const int row0 = " << 4 * R << " * wg;   // first output row of this warp's band\n";
+}
+
+
+// 16-bit planes, staged: the pair's producer (one per pair) keeps one raw plane in flight in its
+// staging buffer (one TMA box, async), widens the previous one into the pair's fp32 slot
+// (LDS.128 -> 2 x STS.128) and claims + issues the next plane right after, so the load latency
+// overlaps the pair's tap loop instead of stalling the producer on its own loads.
+void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, int pass, int es) {
+    const int NB = L.NB, P = L.P;
+    const bool wgrad = pass == 2;
+    const int Win = x.Wo;  // stride 1: input width = output width
+    const size_t raw = (size_t)L.hin * Win * es;
+    const int cpr = Win * es / 16, nch = L.hin * cpr;
+    const int PREF = 2;
+    auto claim = [&](const char *var) {
+        os << "      {\n"
+           << "        int it_ = -1;\n"
+           << "        if (lane == 0) {\n"
+           << "          if (bat < " << NB << " && lo + bat < (unsigned)(nch_of(tcur) * nper)) {\n"
+           << "            it_ = (tcur << 22) | (int)(lo + bat++);\n"
+           << "          } else {\n"
+           << "            bat = " << NB << ";\n"
+           << "            const unsigned v = pf[0];\n"
+           << "            pf[0] = pf[1];\n"
+           << "            const int t0 = tcur;\n"
+           << "            it_ = sched_resolve(p.sched, tcur, v, tried, nper);\n"
+           << "            if (tcur != t0) {\n"
+           << "              pf[0] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+           << "              pf[1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+           << "            } else {\n"
+           << "              pf[1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+           << "            }\n"
+           << "          }\n"
+           << "        }\n"
+           << "        " << var << " = __shfl_sync(0xffffffffu, it_, 0);\n"
+           << "      }\n";
+    };
+    auto issue = [&](const char *var) {  // lane 0: raw plane of item `var` into the staging buffer
+        os << "      if (lane == 0 && " << var << " >= 0) {\n"
+           << "        int t3, c3, n3; item_cn(" << var << ", t3, c3, n3, p.n0);\n"
+           << "        asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(sa(stfull)), \"r\"(" << raw << "u) : \"memory\");\n"
+           << "        tma_load(stage, &p.in_map, 0, 0, c3, n3, stfull, pol);\n"
+           << "      }\n";
+    };
+    os << "  if (warp < " << L.NPROD << ") {\n"
+       << "    const int q = warp;\n"
+       << "    int tcur = 0, tried = 0, bat = 0;\n"
+       << "    const u64 pol = policy_evict_first();\n"
+       << "    const int nper = p.nlen > 0 ? p.nlen : p.N;\n"
+       << "    u64* const stfull = full + 40 + q;\n"
+       << "    unsigned char* const stage = smem + " << L.off_st << " + q * " << L.stb << ";\n"
+       << "    unsigned lo = 0, pf[" << PREF << "];\n"
+       << "    if (lane == 0) {\n"
+       << "      trace_ev(p.trace, 0, -1, trn);\n"
+       << "      tcur = HOME[smid() % NHOME];\n"
+       << "      lo = atomicAdd(p.sched + tcur * CS, " << NB << "u);\n"
+       << "      for (int k = 0; k < " << PREF << "; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << "    }\n"
+       << "    if (!p.nowait) pdl_wait();\n"
+       << "    int nxt;\n";
+    claim("nxt");
+    issue("nxt");
+    os << "    for (int j = 0;; ++j) {\n"
+       << "      const int s = q * " << NB << " + j % " << NB << ";\n"
+       << "      const int item = nxt;\n"
+       << "      if (j >= " << NB << ") mbar_wait(empty + s, ((j / " << NB << ") & 1) ^ 1);\n";
+    if (wgrad) os << "      if (j >= 1) mbar_wait(dyempty + q, ((j - 1) & 1));\n";
+    os << "      int t2 = 0, c2 = 0, n2 = 0;\n"
+       << "      if (item >= 0) item_cn(item, t2, c2, n2, p.n0);\n"
+       << "      if (lane == 0) {\n"
+       << "        s_item[s] = item;\n";
+    if (wgrad)
+        os << "        if (item >= 0) {\n"
+           << "          mbar_expect_tx(full + s, " << (size_t)L.dyp * L.dyrows * es << "u);\n"
+           << "          tma_load(smem + " << L.off_dy << " + q * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s, pol);\n"
+           << "        }\n";
+    os << "      }\n"
+       << "      if (item >= 0) {\n"
+       << "        mbar_wait(stfull, j & 1);\n"
+       << "        float* const dst = reinterpret_cast<float*>(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << ");\n"
+       << "#pragma unroll 4\n"
+       << "        for (int i = lane; i < " << nch << "; i += 32) {\n"
+       << "          const uint4 v = *reinterpret_cast<const uint4*>(stage + i * 16);\n"
+       << "          const int r = i / " << cpr << ", cc = i - r * " << cpr << ";\n"
+       << "          float4* d = reinterpret_cast<float4*>(dst + r * " << L.pitch << " + cc * 8);\n"
+       << "          d[0] = w4(v.x, v.y); d[1] = w4(v.z, v.w);\n"
+       << "        }\n";
+    if (!wgrad)
+        os << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
+    os << "      }\n"
+       << "      __syncwarp();\n"
+       << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");   // staging reads before the next TMA write\n"
+       << "      if (item >= 0) {\n";
+    claim("nxt");
+    issue("nxt");
+    os << "      } else {\n"
+       << "        nxt = -1;\n"
+       << "      }\n"
+       << "      mbar_arrive(full + s);\n"
+       << "      if (item < 0) break;\n"
+       << "    }\n"
+       << "    if (p.nowait) pdl_wait();\n"
+       << "    pdl_trigger();\n"
+       << "    if (lane == 0) sched_exit(p.sched, " << L.NPROD << "u);\n"
+       << "    return;\n"
+       << "  }\n";
+    (void)P;
 }
 
 void emit_loop_head(std::ostringstream &os, const Lay &L) {
@@ -1235,6 +1376,7 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
     os << "extern \"C\" __global__ void __launch_bounds__(" << nthreads << ", 1) " << name << "(const __grid_constant__ Params p) {\n";
     emit_prologue(os, L, pass, es);
     emit_producer(os, x, L, pass, es);
+    emit_consumer_prologue(os, x, L, pass);
     os << "  // -------------------------------------------------------------- consumers\n";
     const std::string ring1 = "reinterpret_cast<const tile_t*>(smem + " + std::to_string(L.off_t + L.zb) + " + s * " +
                               std::to_string(L.zb + L.tb) + ")";
@@ -2250,7 +2392,9 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
     const void *in = pass == 1 ? a.dy : a.x;
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
     const bool cvt = d.dtype != O1D_F32;  // 16-bit rings are widened by the producers (no TMA map)
-    if (cvt) {
+    if (L.staged) {  // raw 16-bit plane, dense box (widened by the producer from its staging buffer)
+        if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, inW, L.hin)) return st;
+    } else if (cvt) {
         hp.cvt1 = in;
         hp.cvt2 = a.dy;
     } else if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, L.pitch, L.hin)) {
