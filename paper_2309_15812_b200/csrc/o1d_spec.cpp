@@ -972,9 +972,8 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << (PQ == 1 ? "        if (j >= " + std::to_string(NB) + ") mbar_wait(empty + s, ((j / " + std::to_string(NB) + ") & 1) ^ 1);\n"
                    : "        if (j >= " + std::to_string(NB) + " && !mbar_test(empty + s, ((j / " + std::to_string(NB) +
                          ") & 1) ^ 1)) continue;   // slot still in use\n");
-    if (wgrad)  // the pair's dy slot is free once it copied the dy block of its previous item
-        os << (PQ == 1 ? "        if (j >= 1) mbar_wait(dyempty + q, ((j - 1) & 1));\n"
-                       : "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n");
+    if (wgrad && PQ != 1)  // the pair's dy slot is free once it copied the dy block of its previous item
+        os << "        if (j >= 1 && !mbar_test(dyempty + q, ((j - 1) & 1))) continue;\n";
     os << "        int item = -1;\n"
        << "        if (lane == 0) {\n"
        << "          if (bat < " << PQ * NB << " && lo + bat < (unsigned)(nch_of(tcur) * nper)) {\n"
@@ -1003,7 +1002,12 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "            trace_ev(p.trace, 1, item, trn);\n";
     if (bytes) os << "            mbar_expect_tx(full + s, " << bytes << "u);\n";
     if (!cvt) os << "            tma_load(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << ", &p.in_map, 0, 0, c2, n2, full + s, pol);\n";
-    if (wgrad) os << "            tma_load(smem + " << L.off_dy << " + q * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s, pol);\n";
+    if (wgrad) {
+        // one producer per pair: the x plane goes out as soon as its slot is free; the dy plane
+        // waits (lane 0 only) until the pair has copied its previous dy block to registers
+        if (PQ == 1) os << "            if (j >= 1) mbar_wait(dyempty + q, ((j - 1) & 1));\n";
+        os << "            tma_load(smem + " << L.off_dy << " + q * " << L.db << ", &p.out_map, 0, 0, c2, n2, full + s, pol);\n";
+    }
     if (fused && !cvt)
         os << "            tma_load(smem + " << L.off_t2 + L.zb2 << " + s * " << L.zb2 + L.tb2 << ", &p.aux_map, 0, 0, c2, n2, full + s, pol);\n";
     os << "          }\n"
