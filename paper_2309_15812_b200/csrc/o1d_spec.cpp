@@ -291,6 +291,7 @@ struct SmallLay {
     bool tma = false;              // inputs by one TMA box per item, plane-major, 4-pixel (16-byte) units
     int UPi = 2;                   // pixels per input unit
     int ustr = 0, lstr = 0;        // input slots: bytes between units of one plane / between planes (lanes)
+    bool tma_out = false;          // stencil outputs staged plane-major and written by one TMA box store
     int hp_in = 0, hp_dy = 0, hp_out = 0;  // units per plane: input, dy (backward_weight), output
     size_t slotb = 0, dyb = 0, outb = 0;
     size_t off_item = 0, off_w = 0, off_slot = 0, off_out = 0, total = 0;
@@ -1179,7 +1180,12 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
        << "          const uint4 v = *reinterpret_cast<const uint4*>(stage + i * 16);\n"
        << "          const int r = i / " << cpr << ", cc = i - r * " << cpr << ";\n"
        << "          float4* d = reinterpret_cast<float4*>(dst + r * " << L.pitch << " + cc * 8);\n"
-       << "          d[0] = w4(v.x, v.y); d[1] = w4(v.z, v.w);\n"
+       // the two 16-byte halves in a lane-dependent order: eight consecutive lanes (chunks 32 B
+       // apart) then hit eight distinct 16-byte bank groups in each store instruction
+       << "          const float4 lo4 = w4(v.x, v.y), hi4 = w4(v.z, v.w);\n"
+       << "          const bool sw = (i >> 2) & 1;\n"
+       << "          d[sw] = sw ? hi4 : lo4;\n"
+       << "          d[!sw] = sw ? lo4 : hi4;\n"
        << "        }\n";
     if (!wgrad)
         os << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
@@ -1547,7 +1553,7 @@ long emit_unit_stream(std::ostringstream &os, const std::map<int, std::vector<st
 // stencil code of one (table, block position): outputs a<r>_<s> of this lane's plane, stored
 // into the quad's output staging (`ob`, unit-major like the input slots) when complete
 long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, int Hin, int Win, int Ho, int Wo, int UB,
-                        int ustr, int UP, const char *ind) {
+                        int ustr, int UP, bool pm_out, const char *ind) {
     long cost = 0;
     const int nd = (int)g.taps.size();
     const auto outs = small_outs(br, bc, Ho, Wo);
@@ -1612,6 +1618,13 @@ long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, in
         for (size_t q = 0; q < t.size(); ++q) os << (q ? " + " : "") << t[q];
         os << ";\n";
     }
+    if (pm_out) {  // plane-major staging (this lane's plane at ob): one fp32 store per output
+        for (auto &o : outs) {
+            os << ind << "*reinterpret_cast<float*>(ob + " << (o.oy * Wo + o.ox) * 4 << ") = a" << o.r << "_" << o.s << ";\n";
+            ++cost;
+        }
+        return cost;
+    }
     // outputs -> staging: pairs of one output unit held by this lane go out as one store
     std::map<int, std::pair<std::string, std::string>> ou;  // output unit -> (lo, hi) value names
     for (auto &o : outs) {
@@ -1666,49 +1679,88 @@ long emit_small_wgrad(std::ostringstream &os, const Geo &g, int br, int bc, int 
     };
     auto gn = [](const SmallOut &o) { return "g" + std::to_string(o.r) + "_" + std::to_string(o.s); };
     std::set<std::pair<int, int>> gpairs;  // (r, s): dy pair (s, s+1) packed once per item
+    std::set<std::pair<int, int>> gbcast;  // (r, s): dy value broadcast to both halves (tap pairs)
+    std::map<std::pair<int, int>, int> tap_at;  // (dh, dw) -> distinct tap
+    for (int d = 0; d < nd; ++d) tap_at[{g.taps[d].dh, g.taps[d].dw}] = d;
+    std::set<std::pair<int, int>> tpairs;  // (d, d2): tap pair accumulators QT<d>_<d2>
+    std::set<std::pair<const SmallOut *, int>> covered;
+    auto pix = [&](const SmallOut &o, int d) {
+        return (o.oy + g.taps[d].dh) * Win + o.ox + g.taps[d].dw;
+    };
+    // 1: output pairs (ox, ox+1), even dw: dy pair x pixel pair into Q<d>
+    for (auto &o : outs)
+        for (int d = 0; d < nd && packed && Wo % 2 == 0; ++d) {
+            if (!inimg(o, d) || ((g.taps[d].dw % 2) + 2) % 2 != 0 || covered.count({&o, d})) continue;
+            const int e = pix(o, d);
+            if (e % 2 != 0) continue;
+            auto it = at.find({o.r, o.ox + 1});
+            if (it == at.end() || !inimg(*it->second, d)) continue;
+            covered.insert({&o, d}), covered.insert({it->second, d});
+            used[d] = upair[d] = true;
+            gpairs.insert({o.r, o.s});
+            const std::string acc = "Q" + std::to_string(d);
+            fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = ffma2(@, GP" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", " + acc + ");", 2}});
+        }
+    // 2: tap pairs (d, d2 = d + (0, 1)) of one output: pixel pair x broadcast dy into QT<d>_<d2>
+    std::map<int, std::vector<std::pair<std::string, bool>>> tpart;  // d -> (QT name, hi half?)
+    for (auto &o : outs)
+        for (int d = 0; d < nd && packed; ++d) {
+            if (!inimg(o, d) || covered.count({&o, d})) continue;
+            const int e = pix(o, d);
+            if (e % 2 != 0) continue;
+            auto it = tap_at.find({g.taps[d].dh, g.taps[d].dw + 1});
+            if (it == tap_at.end()) continue;
+            const int d2 = it->second;
+            if (!inimg(o, d2) || covered.count({&o, d2})) continue;
+            covered.insert({&o, d}), covered.insert({&o, d2});
+            used[d] = used[d2] = true;
+            gbcast.insert({o.r, o.s});
+            const std::string acc = "QT" + std::to_string(d) + "_" + std::to_string(d2);
+            if (tpairs.insert({d, d2}).second) {
+                tpart[d].push_back({acc, false});
+                tpart[d2].push_back({acc, true});
+            }
+            fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = ffma2(@, GB" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", " + acc + ");", 2}});
+        }
+    // 3: the rest, scalar FMAs into q<d>
     for (auto &o : outs)
         for (int d = 0; d < nd; ++d) {
-            if (!inimg(o, d)) continue;
-            used[d] = true;
-            const int h = o.oy + g.taps[d].dh, w = o.ox + g.taps[d].dw;
-            const int e = h * Win + w;
-            // (pairs only where the dy pair is aligned too: ox even, i.e. even dw -- an odd-dw pair
-            // would need its dy pair re-packed, which ptxas rematerialises at every use)
-            if (packed && Wo % 2 == 0 && ((g.taps[d].dw % 2) + 2) % 2 == 0) {
-                const bool lo = (w % 2 + 2) % 2 == 0;
-                auto it = at.find({o.r, lo ? o.ox + 1 : o.ox - 1});
-                if (it != at.end() && inimg(*it->second, d)) {
-                    if (!lo) continue;
-                    upair[d] = true;
-                    gpairs.insert({o.r, o.s});
-                    const std::string acc = "Q" + std::to_string(d);
-                    fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = ffma2(@, GP" + std::to_string(o.r) + "_" + std::to_string(o.s) + ", " + acc + ");", 2}});
-                    continue;
-                }
-            }
-            uscal[d] = true;
+            if (!inimg(o, d) || covered.count({&o, d})) continue;
+            used[d] = uscal[d] = true;
+            const int e = pix(o, d);
             const std::string acc = "q" + std::to_string(d);
             fm[e / UP].push_back({e % UP, UnitFma{acc, acc + " = fmaf(" + gn(o) + ", @, " + acc + ");", 1}});
         }
     for (auto &rs : gpairs)
         os << ind << "const u64 GP" << rs.first << "_" << rs.second << " = f2pack(g" << rs.first << "_" << rs.second << ", g"
            << rs.first << "_" << rs.second + 1 << ");\n";
+    for (auto &rs : gbcast)
+        os << ind << "const u64 GB" << rs.first << "_" << rs.second << " = f2pack(g" << rs.first << "_" << rs.second << ", g"
+           << rs.first << "_" << rs.second << ");\n";
     for (int d = 0; d < nd; ++d) {
         if (upair[d]) os << ind << "u64 Q" << d << " = 0ull;\n";
         if (uscal[d]) os << ind << "float q" << d << " = 0.f;\n";
     }
+    for (auto &tp : tpairs) os << ind << "u64 QT" << tp.first << "_" << tp.second << " = 0ull;\n";
     cost += emit_unit_stream(os, fm, Win, "xb", ustr, UP, ind);
-    for (int d = 0; d < nd; ++d)
-        if (upair[d]) os << ind << (uscal[d] ? "q" : "const float q") << d << (uscal[d] ? " += " : " = ") << "f2lo(Q" << d
-                         << ") + f2hi(Q" << d << ");\n";
+    for (int d = 0; d < nd; ++d) {
+        if (!used[d]) continue;
+        std::vector<std::string> t;
+        if (uscal[d]) t.push_back("q" + std::to_string(d));
+        if (upair[d]) t.push_back("f2lo(Q" + std::to_string(d) + ") + f2hi(Q" + std::to_string(d) + ")");
+        for (auto &tp : tpart[d]) t.push_back((tp.second ? "f2hi(" : "f2lo(") + tp.first + ")");
+        os << ind << "const float qs" << d << " = ";
+        for (size_t i = 0; i < t.size(); ++i) os << (i ? " + " : "") << t[i];
+        os << ";\n";
+    }
     std::vector<bool> written(K, false);
     for (int d = 0; d < nd; ++d) {
         if (!used[d]) continue;
         for (auto &kc : g.taps[d].ks) {
             os << ind << "v[" << kc.first << "] " << (written[kc.first] ? "+= " : "= ");
             written[kc.first] = true;
-            if (kc.second == 1.0f) os << "q" << d << ";\n";
-            else os << flit(kc.second) << " * q" << d << ";\n";
+            if (kc.second == 1.0f) os << "qs" << d << ";\n";
+            else os << flit(kc.second) << " * qs" << d << ";\n";
         }
     }
     for (int k = 0; k < K; ++k)
@@ -1737,7 +1789,8 @@ bool make_small_lay(SmallLay *out, int pass, int H, int W, int Ho, int Wo, int N
     auto rnd = [](size_t b) { return (b + 127) & ~(size_t)127; };
     L.slotb = rnd(L.tma ? (size_t)32 * Hin * Win * 4 : (size_t)L.hp_in * kSmallLanes * L.UB);
     L.dyb = L.hp_dy ? rnd(L.tma ? (size_t)32 * Ho * Wo * 4 : (size_t)L.hp_dy * kSmallLanes * L.UB) : 0;
-    L.outb = L.hp_out ? rnd((size_t)L.hp_out * kSmallLanes * L.UB) : 0;
+    L.tma_out = pass <= 1 && es == 4 && L.hp_out % 2 == 0 && 2 * L.hp_out <= 256 && env_int("O1D_SMALL_TMA", 1);
+    L.outb = L.hp_out ? rnd(L.tma_out ? (size_t)32 * 2 * L.hp_out * 4 : (size_t)L.hp_out * kSmallLanes * L.UB) : 0;
     const size_t budget = (size_t)227 * 1024 - 64;
     for (int NQ = std::max(1, 8 / L.QW); NQ >= 1; --NQ) {
         for (int NB = 3; NB >= 2; --NB) {
@@ -1803,7 +1856,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         for (int bp = 0; bp < QW; ++bp) {
             std::ostringstream b;
             const int br = bp / L.BCs, bc = bp % L.BCs;
-            long c = pass <= 1 ? emit_small_stencil(b, geo[t], br, bc, Hin, Win, Hout, Wout, L.UB, L.ustr, L.UPi, "      ")
+            long c = pass <= 1 ? emit_small_stencil(b, geo[t], br, bc, Hin, Win, Hout, Wout, L.UB, L.ustr, L.UPi, L.tma_out, "      ")
                                : emit_small_wgrad(b, geo[t], br, bc, Hin, Win, x.Ho, x.Wo, K, L.ustr, L.UPi, "      ");
             (*cost_out)[t] += c;
             body.push_back(b.str());
@@ -1829,6 +1882,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
        << "    unsigned pf0 = 0u, pf1 = 0u;\n"
        << "    const u64 pol = policy_evict_first();\n"
        << "    if (lane == 0) {\n"
+       << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = HOME[smid() % NHOME];\n"
        << "      pf0 = atomicAdd(p.sched + tcur * CS, 1u);\n"
        << "      pf1 = atomicAdd(p.sched + tcur * CS, 1u);\n"
@@ -1850,6 +1904,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
        << "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
        << "        }\n"
        << "        s_item[s] = item;\n"
+       << "        if (item >= 0) trace_ev(p.trace, 1, item, trn);\n"
        << "      }\n"
        << "      item = __shfl_sync(0xffffffffu, item, 0);\n"
        << "      if (item >= 0) {\n"
@@ -1897,25 +1952,35 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
        // ------------------------------------------------------------------ consumers
        << "  const int cw = warp - " << NQ << ", q = cw / " << QW << ", bp = cw % " << QW << ";\n";
     if (pass <= 1)
-        os << "  unsigned char* const ob = smem + " << L.off_out << " + q * " << L.outb << " + lane * " << L.UB << ";\n";
+        os << "  unsigned char* const ob = smem + " << L.off_out << " + q * " << L.outb << " + lane * "
+           << (L.tma_out ? Hout * Wout * 4 : L.UB) << ";\n";
     os << "  for (int it = 0;; ++it) {\n"
        << "    const int s = q * " << NB << " + it % " << NB << ";\n"
+       << "    if (lane == 0) trace_ev(p.trace, 2, it, trn);\n"
        << "    mbar_wait(full + s, (it / " << NB << ") & 1);\n"
        << "    const int item = s_item[s];\n"
+       << "    if (lane == 0) trace_ev(p.trace, 3, item, trn);\n"
        << "    if (item < 0) break;\n"
        << "    int t, c, g; item_cn(item, t, c, g, 0);\n"
        << "    const unsigned char* const xb = smem + " << L.off_slot << " + s * " << L.slotb + L.dyb << " + lane * " << L.lstr << ";\n";
     if (pass <= 1) {
         os << "    const float* const wv = wsm + s * 64;\n"
+           << (L.tma_out ? "    if (bp == 0 && lane == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");   // previous box store has read the staging\n" : "")
            << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * QW << ") : \"memory\");   // previous write-back done\n"
            << "    switch (t * " << QW << " + bp) {\n";
         for (size_t i = 0; i < body.size(); ++i) os << "    case " << i << ": {\n" << body[i] << "      break;\n    }\n";
         os << "    }\n"
            << "    __syncwarp();\n"
-           << "    if (lane == 0) mbar_arrive(empty + s);   // input slot free\n"
-           << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * QW << ") : \"memory\");   // all blocks staged\n"
-           // write-back: warp bp stores planes bp, bp + QW, ... (coalesced along each plane)
-           << "    {\n"
+           << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // input slot free\n"
+           << (L.tma_out ? "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");   // staging writes -> the TMA store\n" : "")
+           << "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"(1 + q), \"r\"(" << 32 * QW << ") : \"memory\");   // all blocks staged\n";
+    if (pass <= 1 && L.tma_out) {
+        // one box store: all pixels of the 32 planes (samples past the batch are clipped by the TMA unit)
+        os << "    if (bp == 0 && lane == 0) tma_store_band(&p.out_map, smem + " << L.off_out << " + q * " << L.outb
+           << ", 0, c, 32 * g, policy_evict_first());\n";
+    } else if (pass <= 1) {
+        // write-back: warp bp stores planes bp, bp + QW, ... (coalesced along each plane)
+        os << "    {\n"
            << "      const int HWo = " << Hout * Wout << ";\n"
            << "      unsigned char* const dbase = reinterpret_cast<unsigned char*>(p.dst) + ((u64)(32 * g) * " << x.C
            << " + c) * (u64)HWo * " << L.UB / 2 << ";\n"
@@ -1934,6 +1999,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
            << "        }\n"
            << "      }\n"
            << "    }\n";
+    }
     } else {
         os << "    const unsigned char* const db = xb + " << L.slotb << ";\n"
            << "    float v[" << 32 * NV32 << "];\n"
@@ -1943,7 +2009,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         for (size_t i = 0; i < body.size(); ++i) os << "    case " << i << ": {\n" << body[i] << "      break;\n    }\n";
         os << "    }\n"
            << "    __syncwarp();\n"
-           << "    if (lane == 0) mbar_arrive(empty + s);   // input slot free\n"
+           << "    if (lane == 0) { mbar_arrive(empty + s); trace_ev(p.trace, 4, item, trn); }   // input slot free\n"
            << "    if (32 * g + lane >= p.N) {   // lanes past the batch hold stale planes\n"
            << "#pragma unroll\n"
            << "      for (int k = 0; k < " << 32 * NV32 << "; ++k) v[k] = 0.f;\n"
@@ -1959,8 +2025,10 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
                << "    }\n";
         }
     }
-    os << "  }\n"
-       << "}\n";
+    os << "    if (lane == 0) trace_ev(p.trace, 5, item, trn);\n"
+       << "  }\n";
+    if (pass <= 1 && L.tma_out) os << "  if (bp == 0 && lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
+    os << "}\n";
     if (pass == 2) emit_finalize_ne(os, K, "((N + 31) / 32) * " + std::to_string(QW));
     return os.str();
 }
@@ -2384,6 +2452,10 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
         hp.src1 = pass == 1 ? a.dy : a.x;
         hp.src2 = a.dy;
         hp.dst = pass == 0 ? a.y : a.dx;
+        if (sp->sl[pass].tma_out) {
+            const int hwo = pass == 0 ? pl->P * pl->Q : d.H * d.W;
+            if (o1d_status st = encode(&hp.out_map, hp.dst, d.dtype, hwo, 1, d.C, d.N, hwo, 1, 32)) return st;
+        }
         if (sp->sl[pass].tma) {  // planes as rows of H*W elements: one box = 32 samples of one channel
             const int hwi = pass == 1 ? pl->P * pl->Q : d.H * d.W;
             if (o1d_status st = encode(&hp.in_map, hp.src1, d.dtype, hwi, 1, d.C, d.N, hwi, 1, 32)) return st;

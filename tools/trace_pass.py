@@ -11,8 +11,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--dirs", type=int, default=8)
 ap.add_argument("--K", type=int, default=31)
 ap.add_argument("--angle", type=float, default=None)
+ap.add_argument("--workload", default="s1", choices=["s1", "ks"])
 a = ap.parse_args()
-wl = inputs.S1
+wl = inputs.S1 if a.workload == "s1" else inputs.ksweep(a.K)
 ang = B.direction_angles(a.dirs, wl.C, "cycled") if a.angle is None else np.full(wl.C, a.angle)
 plan = B.Plan(wl.N, wl.C, wl.H, wl.W, a.K, ang, device="cuda:0")
 x = torch.randn(wl.N, wl.C, wl.H, wl.W, device="cuda")
