@@ -22,7 +22,7 @@ namespace o1d {
 namespace {
 
 template <typename T> __device__ __forceinline__ float ld_act(const T *p);
-template <> __device__ __forceinline__ float ld_act<float>(const float *p) { return __ldg(p); }
+template <> __device__ __forceinline__ float ld_act<float>(const float *p) { return *p; }
 template <> __device__ __forceinline__ float ld_act<__nv_bfloat16>(const __nv_bfloat16 *p) {
     return __bfloat162float(*p);
 }
@@ -35,6 +35,45 @@ template <> __device__ __forceinline__ __half to_act<__half>(float v) { return _
 
 constexpr int kThreads = 256;
 constexpr int kSmemBudget = 96 * 1024;
+
+// tile[r][j] = plane[h0 + r][v0 + j] as fp32 (zero outside the Hi x Wi image, reading R1), r < rows,
+// j < cols.  Image rows whose byte length is a multiple of 16 are read in 16-byte vectors (the
+// activations may be 2-byte bf16/fp16: one vector load instead of eight scalar ones).
+template <typename T>
+__device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plane, int Hi, int Wi, int h0, int rows,
+                                           int v0, int cols) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    constexpr int V = 16 / sizeof(T);
+    const bool vec = ((Wi * (int)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(plane) & 15) == 0);
+    if (!vec) {
+        for (int i = tid; i < rows * cols; i += nt) {
+            const int r = i / cols, j = i - r * cols;
+            const int h = h0 + r, v = v0 + j;
+            tile[r * pitch + j] = (h >= 0 && h < Hi && v >= 0 && v < Wi) ? ld_act<T>(plane + (size_t)h * Wi + v) : 0.f;
+        }
+        return;
+    }
+    const int ja = max(0, -v0), jb = min(cols, Wi - v0);  // in-image columns, tile coordinates
+    for (int i = tid; i < rows * cols; i += nt) {          // zero halo (no loads)
+        const int r = i / cols, j = i - r * cols;
+        const int h = h0 + r;
+        if (h < 0 || h >= Hi || j < ja || j >= jb) tile[r * pitch + j] = 0.f;
+    }
+    if (ja >= jb) return;
+    const int ra = max(0, -h0), rb = min(rows, Hi - h0);  // in-image rows
+    const int ma = (v0 + ja) / V, mb = (v0 + jb + V - 1) / V;  // 16-byte chunks covering the columns
+    const int nm = mb - ma;
+    for (int i = tid; i < (rb - ra) * nm; i += nt) {
+        const int rr = i / nm, m = ma + (i - rr * nm), r = ra + rr;
+        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(plane + (size_t)(h0 + r) * Wi) + m);
+        const T *e = reinterpret_cast<const T *>(&u);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const int j = m * V + k - v0;
+            if (j >= ja && j < jb) tile[r * pitch + j] = ld_act<T>(e + k);
+        }
+    }
+}
 
 struct StencilArgs {
     const void *in;
@@ -69,11 +108,7 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     const T *in = static_cast<const T *>(a.in) + (size_t)plane * a.Hi * a.Wi;
     const int h0 = a.str * p0 + a.minDH;
     const int rows = a.str * (nrows - 1) + 1 + (a.maxDH - a.minDH);
-    for (int i = tid; i < rows * a.tileCols; i += blockDim.x) {
-        const int r = i / a.tileCols, j = i - r * a.tileCols;
-        const int h = h0 + r, v = a.minDW + j;
-        tile[r * a.pitch + j] = (h >= 0 && h < a.Hi && v >= 0 && v < a.Wi) ? ld_act<T>(in + (size_t)h * a.Wi + v) : 0.f;
-    }
+    stage_tile<T>(tile, a.pitch, in, a.Hi, a.Wi, h0, rows, a.minDW, a.tileCols);
     __syncthreads();
     T *out = static_cast<T *>(a.out) + (size_t)plane * a.Ho * a.Wo;
     const int qg = (a.Wo + 3) >> 2;
@@ -123,6 +158,71 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_kernel(const T *dy
     dx[i] = to_act<T>(acc);
 }
 
+// Strided backward_input, tiled: one CTA per (plane, band of dx rows); the dy rows and columns the
+// band can reach are staged in shared memory (zero outside), then every thread produces 4
+// consecutive dx outputs of a row: dx[h][w] = sum_e dy[(h-oh_e)/s][(w-ow_e)/s] c_e w_{k_e} over the
+// taps with s | h-oh_e and s | w-ow_e (the divisibility test of a row is shared by the 4 outputs).
+struct BwdInArgs {
+    const void *dy;
+    const float *w;
+    void *dx;
+    const int16_t *oh, *ow, *ek;
+    const float *coef;
+    int C, H, W, P, Q, str, K, KE;
+    int minOH, maxOH, minOW, maxOW;
+    int band, bands;
+    int tileRows, tileCols, pitch;  // dy tile
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdInArgs a) {
+    extern __shared__ float sm[];
+    const int tid = threadIdx.x;
+    const int plane = blockIdx.x / a.bands;
+    const int bnd = blockIdx.x - plane * a.bands;
+    const int c = plane % a.C;
+    const int hb = bnd * a.band, nrows = min(a.band, a.H - hb);
+    const int s = a.str;
+    // dy rows a with hb - maxOH <= s*a <= hb + nrows - 1 - minOH: a0 = ceil((hb - maxOH) / s)
+    const int an = hb - a.maxOH;
+    const int a0 = an >= 0 ? (an + s - 1) / s : -((-an) / s);
+    const int bn = -a.maxOW;
+    const int b0 = bn >= 0 ? (bn + s - 1) / s : -((-bn) / s);
+    float *tile = sm;
+    int *toff = reinterpret_cast<int *>(tile + a.tileRows * a.pitch);
+    float *wk = reinterpret_cast<float *>(toff + a.KE);
+    for (int e = tid; e < a.KE; e += blockDim.x) {
+        const int i = c * a.KE + e;
+        wk[e] = a.coef[i] * a.w[c * a.K + a.ek[i]];
+    }
+    const T *dy = static_cast<const T *>(a.dy) + (size_t)plane * a.P * a.Q;
+    stage_tile<T>(tile, a.pitch, dy, a.P, a.Q, a0, a.tileRows, b0, a.tileCols);
+    __syncthreads();
+    T *dx = static_cast<T *>(a.dx) + (size_t)plane * a.H * a.W;
+    const int qg = (a.W + 3) >> 2;
+    for (int g = tid; g < nrows * qg; g += blockDim.x) {
+        const int hr = g / qg, w0 = (g - hr * qg) * 4, h = hb + hr;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int e = 0; e < a.KE; ++e) {
+            const int i = c * a.KE + e;
+            const int num = h - a.oh[i] - s * a0;  // >= 0 inside the staged rows
+            if (num < 0 || num % s) continue;
+            const float *row = tile + (num / s) * a.pitch;
+            const float wv = wk[e];
+            const int ow = a.ow[i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cn = w0 + j - ow - s * b0;
+                if (cn >= 0 && cn % s == 0 && (cn / s) < a.tileCols) acc[j] = fmaf(row[cn / s], wv, acc[j]);
+            }
+        }
+        T *o = dx + (size_t)h * a.W + w0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (w0 + j < a.W) o[j] = to_act<T>(acc[j]);
+    }
+}
+
 struct BwdWArgs {
     const void *x, *dy;
     float *ws;
@@ -169,12 +269,8 @@ __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a
     const T *dy = static_cast<const T *>(a.dy) + (size_t)plane * a.P * a.Q + (size_t)p0 * a.Q;
     const int h0 = a.str * p0 + a.minOH;
     const int rows = a.str * (nrows - 1) + 1 + (a.maxOH - a.minOH);
-    for (int i = tid; i < rows * a.tileCols; i += blockDim.x) {
-        const int r = i / a.tileCols, j = i - r * a.tileCols;
-        const int h = h0 + r, v = a.minOW + j;
-        tile[r * a.pitch + j] = (h >= 0 && h < a.H && v >= 0 && v < a.W) ? ld_act<T>(x + (size_t)h * a.W + v) : 0.f;
-    }
-    for (int i = tid; i < nrows * a.Q; i += blockDim.x) sdy[i] = ld_act<T>(dy + i);
+    stage_tile<T>(tile, a.pitch, x, a.H, a.W, h0, rows, a.minOW, a.tileCols);
+    stage_tile<T>(sdy, a.Q, dy - (size_t)p0 * a.Q, a.P, a.Q, p0, nrows, 0, a.Q);
     __syncthreads();
     float *ws = a.ws + (size_t)blockIdx.x * a.K;
     for (int k0 = 0; k0 < a.K; k0 += 32) {
@@ -203,21 +299,32 @@ __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a
 }
 
 // dW[c][k] = sum_{e: k_e = k} coef_e * (sum_n sum_band ws[(n*C + c)*bands + band][e]), f64 accumulation,
-// fixed order (rotation / shear: one e per k with coef 1)
-__global__ void bwd_weight_finalize_kernel(const float *ws, float *dW, const int16_t *ek, const float *coef, int N,
-                                           int C, int K, int KE, int bands) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= C * K) return;
-    const int c = i / K, k = i - c * K;
+// fixed order (rotation / shear: one e per k with coef 1).  One CTA per (c, k): thread t sums the
+// entries t, t + 256, ... in order, then a fixed-shape tree over the threads -- deterministic.
+__global__ void __launch_bounds__(256) bwd_weight_finalize_kernel(const float *ws, float *dW, const int16_t *ek,
+                                                                  const float *coef, int N, int C, int K, int KE,
+                                                                  int bands) {
+    __shared__ double red[256];
+    const int c = blockIdx.x / K, k = blockIdx.x - c * K, t = threadIdx.x;
+    const int ne = N * bands;
     double acc = 0.0;
     for (int e = 0; e < KE; ++e) {
-        if (ek[c * KE + e] != k || coef[c * KE + e] == 0.0f) continue;
+        if (ek[c * KE + e] != k || coef[c * KE + e] == 0.0f) continue;  // uniform over the block
         double s = 0.0;
-        for (int n = 0; n < N; ++n)
-            for (int b = 0; b < bands; ++b) s += (double)ws[((size_t)(n * C + c) * bands + b) * KE + e];
-        acc += (double)coef[c * KE + e] * s;
+        for (int i = t; i < ne; i += 256) {
+            const int n = i / bands, b = i - n * bands;
+            s += (double)ws[((size_t)(n * C + c) * bands + b) * KE + e];
+        }
+        red[t] = s;
+        __syncthreads();
+        for (int h = 128; h > 0; h >>= 1) {
+            if (t < h) red[t] += red[t + h];
+            __syncthreads();
+        }
+        if (t == 0) acc += (double)coef[c * KE + e] * red[0];
+        __syncthreads();
     }
-    dW[i] = (float)acc;
+    if (t == 0) dW[blockIdx.x] = (float)acc;
 }
 
 o1d_status check_launch(const char *what) {
@@ -285,6 +392,36 @@ o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, cons
 
 o1d_status generic_bwd_input_strided(const o1d_plan *pl, const void *dy, const float *w, void *dx, void *stream) {
     const o1d_desc &d = pl->d;
+    {
+        // tiled path: the dy rows / columns a band of dx rows can reach, staged in shared memory
+        BwdInArgs a;
+        a.dy = dy; a.w = w; a.dx = dx; a.oh = pl->d_oh; a.ow = pl->d_ow; a.ek = pl->d_ek; a.coef = pl->d_coef;
+        a.C = d.C; a.H = d.H; a.W = d.W; a.P = pl->P; a.Q = pl->Q; a.str = d.stride; a.K = d.K; a.KE = pl->KE;
+        a.minOH = pl->minOH; a.maxOH = pl->maxOH; a.minOW = pl->minOW; a.maxOW = pl->maxOW;
+        const int s = d.stride;
+        a.tileCols = (d.W - 1 + a.maxOW - a.minOW) / s + 2;
+        a.pitch = a.tileCols + ((a.tileCols & 31) == 0 ? 1 : 0);
+        int band = d.H;
+        auto rows_for = [&](int b) { return (b - 1 + a.maxOH - a.minOH) / s + 2; };
+        auto smem_for = [&](int b) { return sizeof(float) * ((size_t)rows_for(b) * a.pitch + 2 * a.KE); };
+        while (band > 1 && smem_for(band) > (size_t)kSmemBudget) band = (band + 1) / 2;
+        if (smem_for(band) <= (size_t)kSmemBudget) {
+            a.band = band;
+            a.bands = (d.H + band - 1) / band;
+            a.tileRows = rows_for(band);
+            const size_t smem = smem_for(band);
+            const long grid = (long)d.N * d.C * a.bands;
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            return dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
+                using T = decltype(tag);
+                auto kern = bwd_input_strided_tiled_kernel<T>;
+                if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                    return check_launch("bwd_input_strided_tiled attr");
+                kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
+                return check_launch("bwd_input_strided_tiled");
+            });
+        }
+    }
     const long total = (long)d.N * d.C * d.H * d.W;
     const unsigned grid = (unsigned)((total + kThreads - 1) / kThreads);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -319,9 +456,7 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
         return check_launch("bwd_weight_generic");
     });
     if (r != O1D_OK) return r;
-    const int n = d.C * d.K;
-    bwd_weight_finalize_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, dW, pl->d_ek, pl->d_coef, d.N, d.C, d.K, pl->KE,
-                                                               a.bands);
+    bwd_weight_finalize_kernel<<<d.C * d.K, 256, 0, s>>>(ws, dW, pl->d_ek, pl->d_coef, d.N, d.C, d.K, pl->KE, a.bands);
     return check_launch("bwd_weight_finalize");
 }
 
