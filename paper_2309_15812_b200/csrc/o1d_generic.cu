@@ -54,25 +54,69 @@ __device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plan
         return;
     }
     const int ja = max(0, -v0), jb = min(cols, Wi - v0);  // in-image columns, tile coordinates
-    for (int i = tid; i < rows * cols; i += nt) {          // zero halo (no loads)
-        const int r = i / cols, j = i - r * cols;
-        const int h = h0 + r;
-        if (h < 0 || h >= Hi || j < ja || j >= jb) tile[r * pitch + j] = 0.f;
+    if (ja >= jb) {
+        for (int i = tid; i < rows * cols; i += nt) tile[(i / cols) * pitch + i % cols] = 0.f;
+        return;
     }
-    if (ja >= jb) return;
-    const int ra = max(0, -h0), rb = min(rows, Hi - h0);  // in-image rows
-    const int ma = (v0 + ja) / V, mb = (v0 + jb + V - 1) / V;  // 16-byte chunks covering the columns
-    const int nm = mb - ma;
-    for (int i = tid; i < (rb - ra) * nm; i += nt) {
-        const int rr = i / nm, m = ma + (i - rr * nm), r = ra + rr;
-        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(plane + (size_t)(h0 + r) * Wi) + m);
-        const T *e = reinterpret_cast<const T *>(&u);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const int j = m * V + k - v0;
-            if (j >= ja && j < jb) tile[r * pitch + j] = ld_act<T>(e + k);
+    {  // zero halo (no loads): whole rows outside the image, the side columns of the others
+        const int side = ja + (cols - jb);
+        for (int i = tid; i < rows * side; i += nt) {
+            const int r = i / side, k = i - r * side;
+            const int h = h0 + r;
+            if (h < 0 || h >= Hi) continue;
+            tile[r * pitch + (k < ja ? k : jb + (k - ja))] = 0.f;
+        }
+        const int ra0 = max(0, -h0), rb0 = max(ra0, min(rows, Hi - h0));
+        const int nout = ra0 + (rows - rb0);  // rows outside the image: [0, ra0) and [rb0, rows)
+        for (int i = tid; i < nout * cols; i += nt) {
+            const int k = i / cols, r = k < ra0 ? k : rb0 + (k - ra0);
+            tile[r * pitch + (i - k * cols)] = 0.f;
         }
     }
+    const int ra = max(0, -h0), rb = min(rows, Hi - h0);  // in-image rows
+    const int ma = (v0 + ja) / V, mb = (v0 + jb + V - 1) / V;  // 16-byte chunks covering the columns
+    const int nm = mb - ma, total = (rb - ra) * nm;
+    constexpr int U = 4;  // four independent 16-byte loads in flight per thread
+    for (int i0 = tid; i0 < total; i0 += U * nt) {
+        uint4 u[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int i = i0 + q * nt;
+            if (i < total) {
+                const int rr = i / nm, m = ma + (i - rr * nm);
+                u[q] = __ldg(reinterpret_cast<const uint4 *>(plane + (size_t)(h0 + ra + rr) * Wi) + m);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int i = i0 + q * nt;
+            if (i >= total) break;
+            const int rr = i / nm, m = ma + (i - rr * nm), r = ra + rr;
+            const T *e = reinterpret_cast<const T *>(&u[q]);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const int j = m * V + k - v0;
+                if (j >= ja && j < jb) tile[r * pitch + j] = ld_act<T>(e + k);
+            }
+        }
+    }
+}
+
+// four consecutive outputs of a row, packed into one 8- or 16-byte store when aligned
+template <typename T>
+__device__ __forceinline__ void store4(T *o, const float (&acc)[4], int nvalid) {
+    if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & (4 * sizeof(T) - 1)) == 0) {
+        if constexpr (sizeof(T) == 4) {
+            *reinterpret_cast<float4 *>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        } else {
+            T v[4] = {to_act<T>(acc[0]), to_act<T>(acc[1]), to_act<T>(acc[2]), to_act<T>(acc[3])};
+            *reinterpret_cast<uint2 *>(o) = *reinterpret_cast<const uint2 *>(v);
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < nvalid) o[j] = to_act<T>(acc[j]);
 }
 
 struct StencilArgs {
@@ -124,11 +168,8 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
             acc2 = fmaf(s[2 * a.str], wv, acc2);
             acc3 = fmaf(s[3 * a.str], wv, acc3);
         }
-        T *o = out + (size_t)(p0 + pr) * a.Wo + q0;
-        o[0] = to_act<T>(acc0);
-        if (q0 + 1 < a.Wo) o[1] = to_act<T>(acc1);
-        if (q0 + 2 < a.Wo) o[2] = to_act<T>(acc2);
-        if (q0 + 3 < a.Wo) o[3] = to_act<T>(acc3);
+        const float acc[4] = {acc0, acc1, acc2, acc3};
+        store4<T>(out + (size_t)(p0 + pr) * a.Wo + q0, acc, min(4, a.Wo - q0));
     }
 }
 
@@ -174,7 +215,8 @@ struct BwdInArgs {
     int tileRows, tileCols, pitch;  // dy tile
 };
 
-template <typename T>
+// SC: the stride as a compile-time constant (2: the Depthwise 1D Stem) or 0 (run time)
+template <typename T, int SC>
 __global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdInArgs a) {
     extern __shared__ float sm[];
     const int tid = threadIdx.x;
@@ -182,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdIn
     const int bnd = blockIdx.x - plane * a.bands;
     const int c = plane % a.C;
     const int hb = bnd * a.band, nrows = min(a.band, a.H - hb);
-    const int s = a.str;
+    const int s = SC ? SC : a.str;
     // dy rows a with hb - maxOH <= s*a <= hb + nrows - 1 - minOH: a0 = ceil((hb - maxOH) / s)
     const int an = hb - a.maxOH;
     const int a0 = an >= 0 ? (an + s - 1) / s : -((-an) / s);
@@ -216,10 +258,7 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdIn
                 if (cn >= 0 && cn % s == 0 && (cn / s) < a.tileCols) acc[j] = fmaf(row[cn / s], wv, acc[j]);
             }
         }
-        T *o = dx + (size_t)h * a.W + w0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (w0 + j < a.W) o[j] = to_act<T>(acc[j]);
+        store4<T>(dx + (size_t)h * a.W + w0, acc, min(4, a.W - w0));
     }
 }
 
@@ -414,7 +453,7 @@ o1d_status generic_bwd_input_strided(const o1d_plan *pl, const void *dy, const f
             cudaStream_t st = static_cast<cudaStream_t>(stream);
             return dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
                 using T = decltype(tag);
-                auto kern = bwd_input_strided_tiled_kernel<T>;
+                auto kern = s == 2 ? bwd_input_strided_tiled_kernel<T, 2> : bwd_input_strided_tiled_kernel<T, 0>;
                 if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                     return check_launch("bwd_input_strided_tiled attr");
                 kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
