@@ -519,3 +519,26 @@ def test_small_planes_angle_sets(angle_set):
 def test_small_planes_discretizations(disc):
     angles = B.direction_angles(8, 16, "cycled")
     run_case(35, 16, 14, 14, 31, angles, disc=disc, expect="spec-small")
+
+
+@pytest.mark.parametrize("shape", [(2, 16, 56, 56, 31), (33, 16, 14, 14, 31), (3, 8, 40, 48, 15), (70, 16, 14, 14, 63)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_outputs_fully_written(shape, dtype):
+    """Every output element is written by the kernels (the TMA box/band stores included: the
+    compute-sanitizer initcheck does not track bulk-async writes, profiles/r2/sanitizer_r2.txt):
+    outputs pre-filled with NaN come back finite and dW is overwritten, never accumulated."""
+    N, C, H, W, K = shape
+    plan = B.Plan(N, C, H, W, K, B.direction_angles(8, C, "cycled"), dtype=dtype, device="cuda:0")
+    assert plan.describe().startswith("spec"), plan.describe()
+    x = torch.randn(N, C, H, W, device="cuda").to(dtype)
+    dy = torch.randn(N, C, plan.P, plan.Q, device="cuda").to(dtype)
+    w = torch.randn(C, K, device="cuda")
+    y = torch.full_like(dy, float("nan"))
+    dx = torch.full_like(x, float("nan"))
+    dW = torch.full_like(w, float("nan"))
+    ws = torch.full((B.workspace(plan).numel(),), float("nan"), device="cuda")
+    B.forward(plan, x, w, y)
+    B.backward_input(plan, dy, w, dx)
+    B.backward_weight(plan, x, dy, dW, ws)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y.float()).all() and torch.isfinite(dx.float()).all() and torch.isfinite(dW).all()
