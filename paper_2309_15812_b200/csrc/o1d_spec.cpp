@@ -287,7 +287,9 @@ struct Lay {
 struct SmallLay {
     int BRs = 1, BCs = 1, QW = 1;  // 7x7 block positions per plane = warps per quad
     int NQ = 1, NB = 2, G = 1;     // quads, input slots per quad, 32-plane groups per channel
-    int UB = 8;                    // bytes per unit (2 pixels) of the LDGSTS slots and the output staging
+    int UB = 8;                    // bytes per unit (UPu pixels) of the LDGSTS slots and the output staging
+    int UPu = 2, es = 4;           // pixels per unit (1 for odd H*W), activation bytes
+    bool sync_copy = false;        // 16-bit odd planes: 2-byte units copied by plain loads (cp.async moves >= 4 B)
     bool tma = false;              // inputs by one TMA box per item, plane-major, 4-pixel (16-byte) units
     int UPi = 2;                   // pixels per input unit
     int ustr = 0, lstr = 0;        // input slots: bytes between units of one plane / between planes (lanes)
@@ -1453,12 +1455,14 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
 constexpr int kSmallLanes = 33;  // unit stride in a slot: 32 planes + 1 (bank skew)
 
 // unit loads / stores of the unit-major slots (fp32: float2, 16-bit: packed u32)
-void emit_small_header(std::ostringstream &os, int act) {
+void emit_small_header(std::ostringstream &os, int act, int UPu) {
     os << "__device__ __forceinline__ void cp_async_unit(void* dst, const void* src, u64 pol) {\n";
-    if (act == O1D_F32)
-        os << "  asm volatile(\"cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\" :: \"r\"(sa(dst)), \"l\"(src), \"l\"(pol) : \"memory\");\n";
-    else
+    if (UPu == 1 && act != O1D_F32)
+        os << "  *reinterpret_cast<unsigned short*>(dst) = __ldg(reinterpret_cast<const unsigned short*>(src)); (void)pol;\n";
+    else if (UPu == 1 || act != O1D_F32)
         os << "  asm volatile(\"cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\" :: \"r\"(sa(dst)), \"l\"(src), \"l\"(pol) : \"memory\");\n";
+    else
+        os << "  asm volatile(\"cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\" :: \"r\"(sa(dst)), \"l\"(src), \"l\"(pol) : \"memory\");\n";
     os << "}\n"
        << "__device__ __forceinline__ void cp_async_w(void* dst, const void* src) {\n"
        << "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: \"r\"(sa(dst)), \"l\"(src) : \"memory\");\n"
@@ -1466,7 +1470,15 @@ void emit_small_header(std::ostringstream &os, int act) {
        << "__device__ __forceinline__ void cp_async_arrive(u64* b) {\n"
        << "  asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(sa(b)) : \"memory\");\n"
        << "}\n";
-    if (act == O1D_F32)
+    if (UPu == 1 && act == O1D_F32)
+        os << "typedef float unit_t;\n"
+              "__device__ __forceinline__ float ulo(unit_t v) { return v; }\n"
+              "__device__ __forceinline__ float uhi(unit_t v) { return 0.f; }\n";
+    else if (UPu == 1)
+        os << "typedef unsigned short unit_t;\n"
+              "__device__ __forceinline__ float ulo(unit_t v) { return LD(v); }\n"
+              "__device__ __forceinline__ float uhi(unit_t v) { return 0.f; }\n";
+    else if (act == O1D_F32)
         os << "typedef float2 unit_t;\n"
               "__device__ __forceinline__ float ulo(unit_t v) { return v.x; }\n"
               "__device__ __forceinline__ float uhi(unit_t v) { return v.y; }\n"
@@ -1553,7 +1565,7 @@ long emit_unit_stream(std::ostringstream &os, const std::map<int, std::vector<st
 // stencil code of one (table, block position): outputs a<r>_<s> of this lane's plane, stored
 // into the quad's output staging (`ob`, unit-major like the input slots) when complete
 long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, int Hin, int Win, int Ho, int Wo, int UB,
-                        int ustr, int UP, bool pm_out, const char *ind) {
+                        int ustr, int UP, bool pm_out, int UPo, const char *ind) {
     long cost = 0;
     const int nd = (int)g.taps.size();
     const auto outs = small_outs(br, bc, Ho, Wo);
@@ -1563,7 +1575,7 @@ long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, in
     // unit): the outputs (ox, ox+1) of one row take tap d with one FFMA2 when ox + dw is even and
     // both are in the image -- accumulator pairs at even ox ("A") for even dw, at odd ox ("B") for
     // odd dw; every other in-image (output, tap) is a scalar FMA into S_r_s.  a = A + B + S.
-    const bool packed = Win % 2 == 0;
+    const bool packed = Win % 2 == 0 && UP >= 2;
     std::map<std::pair<int, int>, const SmallOut *> at;  // (r, ox) -> output
     for (auto &o : outs) at[{o.r, o.ox}] = &o;
     auto inimg = [&](const SmallOut &o, int d) {
@@ -1629,8 +1641,8 @@ long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, in
     std::map<int, std::pair<std::string, std::string>> ou;  // output unit -> (lo, hi) value names
     for (auto &o : outs) {
         const int e = o.oy * Wo + o.ox;
-        auto &slot = ou[e >> 1];
-        (e & 1 ? slot.second : slot.first) = "a" + std::to_string(o.r) + "_" + std::to_string(o.s);
+        auto &slot = ou[e / UPo];
+        (e % UPo ? slot.second : slot.first) = "a" + std::to_string(o.r) + "_" + std::to_string(o.s);
     }
     for (auto &kv : ou) {
         const size_t off = (size_t)kv.first * kSmallLanes * UB;
@@ -1638,7 +1650,7 @@ long emit_small_stencil(std::ostringstream &os, const Geo &g, int br, int bc, in
         if (!lo.empty() && !hi.empty()) {
             os << ind << "*reinterpret_cast<unit_t*>(ob + " << off << ") = upack(" << lo << ", " << hi << ");\n";
         } else {
-            const int es = UB / 2;
+            const int es = UB / UPo;
             const size_t o2 = off + (lo.empty() ? es : 0);
             os << ind << "*reinterpret_cast<act_t*>(ob + " << o2 << ") = to_act(" << (lo.empty() ? hi : lo) << ");\n";
         }
@@ -1670,7 +1682,7 @@ long emit_small_wgrad(std::ostringstream &os, const Geo &g, int br, int bc, int 
     // packed FP32 (even Win): outputs (ox, ox+1) of one row whose pixels (e, e+1) start at an even
     // e take tap d with one FFMA2 (dy pair x pixel pair) into the pair accumulator Q<d>; the rest
     // are scalar FMAs into q<d>
-    const bool packed = Win % 2 == 0;
+    const bool packed = Win % 2 == 0 && UP >= 2;
     std::map<std::pair<int, int>, const SmallOut *> at;
     for (auto &o : outs) at[{o.r, o.ox}] = &o;
     auto inimg = [&](const SmallOut &o, int d) {
@@ -1774,23 +1786,27 @@ bool make_small_lay(SmallLay *out, int pass, int H, int W, int Ho, int Wo, int N
     L.BRs = (Ho + R - 1) / R;
     L.BCs = (Wo + S - 1) / S;
     L.QW = L.BRs * L.BCs;
-    L.UB = 2 * es;
+    L.es = es;
+    L.UPu = (H * W) % 2 == 0 && (Ho * Wo) % 2 == 0 ? 2 : 1;
+    L.UB = L.UPu * es;
+    L.sync_copy = L.UPu == 1 && es == 2;
     L.G = (N + 31) / 32;
     const int Hin = pass == 1 ? Ho : H, Win = pass == 1 ? Wo : W;
     // fp32 planes whose byte size is a multiple of 16 (and at most 256 elements, one TMA box row)
     // arrive by one TMA box per item; others by per-unit cp.async (LDGSTS)
     L.tma = es == 4 && (Hin * Win) % 4 == 0 && Hin * Win <= 256 && (pass != 2 || (Ho * Wo) % 4 == 0) && env_int("O1D_SMALL_TMA", 1);
-    L.UPi = L.tma ? 4 : 2;
+    L.UPi = L.tma ? 4 : L.UPu;
     L.ustr = L.tma ? 16 : kSmallLanes * L.UB;
     L.lstr = L.tma ? Hin * Win * 4 : L.UB;
-    L.hp_in = Hin * Win / 2;
-    L.hp_dy = pass == 2 ? Ho * Wo / 2 : 0;
-    L.hp_out = pass <= 1 ? (pass == 0 ? Ho * Wo : H * W) / 2 : 0;
+    L.hp_in = Hin * Win / L.UPu;
+    L.hp_dy = pass == 2 ? Ho * Wo / L.UPu : 0;
+    L.hp_out = pass <= 1 ? (pass == 0 ? Ho * Wo : H * W) / L.UPu : 0;
     auto rnd = [](size_t b) { return (b + 127) & ~(size_t)127; };
     L.slotb = rnd(L.tma ? (size_t)32 * Hin * Win * 4 : (size_t)L.hp_in * kSmallLanes * L.UB);
     L.dyb = L.hp_dy ? rnd(L.tma ? (size_t)32 * Ho * Wo * 4 : (size_t)L.hp_dy * kSmallLanes * L.UB) : 0;
-    L.tma_out = pass <= 1 && es == 4 && L.hp_out % 2 == 0 && 2 * L.hp_out <= 256 && env_int("O1D_SMALL_TMA", 1);
-    L.outb = L.hp_out ? rnd(L.tma_out ? (size_t)32 * 2 * L.hp_out * 4 : (size_t)L.hp_out * kSmallLanes * L.UB) : 0;
+    const int hwo = L.hp_out * L.UPu;
+    L.tma_out = pass <= 1 && es == 4 && hwo % 4 == 0 && hwo <= 256 && env_int("O1D_SMALL_TMA", 1);
+    L.outb = L.hp_out ? rnd(L.tma_out ? (size_t)32 * hwo * 4 : (size_t)L.hp_out * kSmallLanes * L.UB) : 0;
     const size_t budget = (size_t)227 * 1024 - 64;
     for (int NQ = std::max(1, 8 / L.QW); NQ >= 1; --NQ) {
         for (int NB = 3; NB >= 2; --NB) {
@@ -1838,7 +1854,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
                            std::vector<long> *cost_out) {
     std::ostringstream os;
     emit_header(os, x);
-    emit_small_header(os, x.act);
+    emit_small_header(os, x.act, L.UPu);
     if (L.tma)
         os << "typedef float4 uin_t;\n#define UPX(v, i) ((i) == 0 ? (v).x : (i) == 1 ? (v).y : (i) == 2 ? (v).z : (v).w)\n";
     else
@@ -1856,7 +1872,7 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         for (int bp = 0; bp < QW; ++bp) {
             std::ostringstream b;
             const int br = bp / L.BCs, bc = bp % L.BCs;
-            long c = pass <= 1 ? emit_small_stencil(b, geo[t], br, bc, Hin, Win, Hout, Wout, L.UB, L.ustr, L.UPi, L.tma_out, "      ")
+            long c = pass <= 1 ? emit_small_stencil(b, geo[t], br, bc, Hin, Win, Hout, Wout, L.UB, L.ustr, L.UPi, L.tma_out, L.UPu, "      ")
                                : emit_small_wgrad(b, geo[t], br, bc, Hin, Win, x.Ho, x.Wo, K, L.ustr, L.UPi, "      ");
             (*cost_out)[t] += c;
             body.push_back(b.str());
@@ -1914,11 +1930,11 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         const int nk = (hp + 31) / 32;
         os << "        {\n"
            << "          const unsigned char* const src = reinterpret_cast<const unsigned char*>(" << src << ") + ((u64)(32 * g) * "
-           << x.C << " + c) * " << (long)HW * (L.UB / 2) << ";\n"
+           << x.C << " + c) * " << (long)HW * L.es << ";\n"
            << "#pragma unroll 1\n"
            << "          for (int jj = 0; jj < 32; ++jj) {\n"
            << "            if (32 * g + jj >= p.N) break;\n"
-           << "            const unsigned char* const pl = src + (u64)jj * " << (long)x.C * HW * (L.UB / 2) << ";\n"
+           << "            const unsigned char* const pl = src + (u64)jj * " << (long)x.C * HW * L.es << ";\n"
            << "#pragma unroll\n"
            << "            for (int k = 0; k < " << nk << "; ++k) {\n"
            << "              const int u = lane + 32 * k;\n"
@@ -1938,10 +1954,15 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         copy_planes("p.src1", Hin * Win, L.hp_in, 0);
         if (pass == 2) copy_planes("p.src2", x.Ho * x.Wo, L.hp_dy, L.slotb);
     }
-    if (pass <= 1)
-        os << "        for (int k = lane; k < " << K << "; k += 32) cp_async_w(wsm + s * 64 + k, p.w + c * " << K << " + k);\n";
+    if (pass <= 1) {
+        if (L.sync_copy)
+            os << "        for (int k = lane; k < " << K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c * " << K << " + k);\n";
+        else
+            os << "        for (int k = lane; k < " << K << "; k += 32) cp_async_w(wsm + s * 64 + k, p.w + c * " << K << " + k);\n";
+    }
     os << "      }\n"
-       << "      cp_async_arrive(full + s);   // 32 lanes: each arrival fires when the lane's copies have landed\n"
+       << (L.sync_copy ? "      mbar_arrive(full + s);   // plain copies: the arrive releases them\n"
+                       : "      cp_async_arrive(full + s);   // 32 lanes: each arrival fires when the lane's copies have landed\n")
        << "      if (item < 0) break;\n"
        << "    }\n"
        << "    if (p.nowait) pdl_wait();\n"
@@ -1983,12 +2004,12 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
         os << "    {\n"
            << "      const int HWo = " << Hout * Wout << ";\n"
            << "      unsigned char* const dbase = reinterpret_cast<unsigned char*>(p.dst) + ((u64)(32 * g) * " << x.C
-           << " + c) * (u64)HWo * " << L.UB / 2 << ";\n"
+           << " + c) * (u64)HWo * " << L.es << ";\n"
            << "      const unsigned char* const obq = smem + " << L.off_out << " + q * " << L.outb << ";\n"
            << "#pragma unroll 1\n"
            << "      for (int jj = bp; jj < 32; jj += " << QW << ") {\n"
            << "        if (32 * g + jj >= p.N) break;\n"
-           << "        unsigned char* const pl = dbase + (u64)jj * " << (long)x.C * Hout * Wout * (L.UB / 2) << ";\n"
+           << "        unsigned char* const pl = dbase + (u64)jj * " << (long)x.C * Hout * Wout * L.es << ";\n"
            << "#pragma unroll\n"
            << "        for (int k = 0; k < " << (L.hp_out + 31) / 32 << "; ++k) {\n"
            << "          const int u = lane + 32 * k;\n"
@@ -2149,7 +2170,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
     const int es = (int)dtype_size(d.dtype);
     if (d.stride != 1) return false;  // stride 2 runs on the generic kernels
     if (d.K > 64 || pl->n_distinct > 16) return false;
-    if (d.H <= 2 * R && d.W <= 2 * S && (d.H * d.W) % 2 == 0 && env_int("O1D_SMALL", 1) != 0)
+    if (d.H <= 2 * R && d.W <= 2 * S && env_int("O1D_SMALL", 1) != 0)
         return small_prepare(pl, sp, src, nsm, gpc);
     if ((d.W * es) % 16 != 0) return false;
     if (pl->n_distinct > 16 || (long)d.N * d.C >= (1L << 22)) return false;

@@ -145,7 +145,7 @@ def test_spec_source_ineligible_shapes():
         B.spec_source(1, 8, 30, 30, 7, np.zeros(8), 0)  # 30*4 B rows: not TMA-legal, too big for small planes
     assert e.value.status == 5
     with pytest.raises(B.O1DError):
-        B.spec_source(1, 8, 7, 7, 7, np.zeros(8), 0)  # odd H*W: no 2-pixel units
+        B.spec_source(1, 8, 15, 15, 7, np.zeros(8), 0)  # 15 > 14 and 60-byte rows: generic kernels
     with pytest.raises(B.O1DError):
         B.spec_source(1, 8, 56, 56, 7, np.zeros(8), 0, stride=2)
 

@@ -502,7 +502,9 @@ def test_torch_library_opcheck():
 @pytest.mark.parametrize("HW,N,K,assign", [((14, 14), 33, 31, "cycled"), ((14, 14), 70, 63, "contiguous"),
                                            ((12, 14), 5, 15, "cycled"), ((8, 8), 40, 7, "contiguous"),
                                            ((6, 4), 3, 31, "cycled"), ((14, 10), 32, 27, "cycled"),
-                                           ((2, 2), 2, 7, "cycled"), ((7, 14), 9, 31, "contiguous")])
+                                           ((2, 2), 2, 7, "cycled"), ((7, 14), 9, 31, "contiguous"),
+                                           ((7, 7), 70, 15, "contiguous"), ((7, 9), 33, 31, "cycled"),
+                                           ((5, 3), 4, 7, "cycled"), ((1, 1), 3, 5, "cycled")])
 def test_small_planes(dtype, HW, N, K, assign):
     C = 16
     angles = B.direction_angles(8, C, assign)
