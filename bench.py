@@ -347,6 +347,52 @@ def run_model(args):
                        "image": 224, "oriented_layers": n_or, "optimizer": "AdamW",
                        "parallelism": f"ddp{world} (NCCL all-reduce of every gradient incl. dW)"},
             "clocks": ck, "loss": float(loss.item())}
+    if rank == 0 and world == 1:
+        # share of the step's GPU kernel time in liboriented1d's kernels (torch.profiler, 2 steps
+        # after the timed region)
+        try:
+            with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+                for i in range(2):
+                    step(i)
+                torch.cuda.synchronize()
+            tot = ours = 0.0
+            for e in prof.events():
+                if e.device_type == torch.autograd.DeviceType.CUDA:
+                    dt_ = getattr(e, "device_time_total", 0.0)
+                    tot += dt_
+                    if "o1d" in e.name:
+                        ours += dt_
+            line["oriented_share"] = {"kernel_time_frac": ours / tot if tot else None,
+                                      "oriented_ms_per_step": ours / 2 / 1e3, "kernel_ms_per_step": tot / 2 / 1e3,
+                                      "how": "torch.profiler CUDA kernel time, kernels of liboriented1d vs all"}
+        except Exception as ex_:  # pragma: no cover
+            line["oriented_share"] = {"error": repr(ex_)}
+        # comparator: the same network with torch's 1xK depthwise conv2d (cuDNN) in
+        # place of every oriented layer, timed the same way
+        try:
+            del opt, model
+            torch.cuda.empty_cache()
+            ref = convnext1d.ConvNeXt1D(args.model, impl="torch1xk").to(dev).to(torch.bfloat16)
+            ropt = torch.optim.AdamW(ref.parameters(), lr=1e-4)
+
+            def rstep(i):
+                ropt.zero_grad(set_to_none=True)
+                torch.nn.functional.cross_entropy(ref(imgs[i & 1]).float(), labels[i & 1]).backward()
+                ropt.step()
+            for i in range(args.warmup):
+                rstep(i)
+            torch.cuda.synchronize()
+            t0.record()
+            for i in range(args.steps):
+                rstep(i)
+            t1.record()
+            torch.cuda.synchronize()
+            rms = t0.elapsed_time(t1) / args.steps
+            line["comparator"] = {"what": "same network, torch depthwise conv2d 1xK (cuDNN) instead of the oriented layers",
+                                  "images_per_s": B / (rms * 1e-3), "ms_per_step": rms,
+                                  "oriented_over_1xk": (B / (ms * 1e-3)) / (B / (rms * 1e-3))}
+        except Exception as ex_:  # pragma: no cover
+            line["comparator"] = {"error": repr(ex_)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -34,6 +34,17 @@ CONFIGS = {
 STAGE_K = (31, 31, 27, 15)
 
 
+def make_dw(C, K, angles=None, D=8, stride=1, shift_deg=0.0, impl="oriented"):
+    """The depthwise layer of a block / the stem: the oriented 1D conv (liboriented1d), or -- as
+    the comparator of PAPER.md:1027 ("1xK" PyTorch depthwise conv) -- torch's depthwise conv2d
+    with a horizontal 1xK kernel of the same length and stride (cuDNN), same surrounding network."""
+    if impl == "torch1xk":
+        return nn.Conv2d(C, C, (1, K), stride=stride, padding=(0, K // 2), groups=C, bias=False)
+    if angles is not None:
+        return Oriented1dDWConv(C, K, angles_deg=angles, stride=stride)
+    return Oriented1dDWConv(C, K, D=D, assign="contiguous", shift_deg=shift_deg, stride=stride)
+
+
 class LayerNorm2d(nn.Module):
     """LayerNorm over channels of an NCHW tensor."""
 
@@ -46,9 +57,9 @@ class LayerNorm2d(nn.Module):
 
 
 class Block1D(nn.Module):
-    def __init__(self, C, K, D, shift_deg):
+    def __init__(self, C, K, D, shift_deg, impl="oriented"):
         super().__init__()
-        self.dw = Oriented1dDWConv(C, K, D=D, assign="contiguous", shift_deg=shift_deg)
+        self.dw = make_dw(C, K, D=D, shift_deg=shift_deg, impl=impl)
         self.norm = nn.LayerNorm(C, eps=1e-6)
         self.pw1 = nn.Linear(C, 4 * C)
         self.pw2 = nn.Linear(4 * C, C)
@@ -61,14 +72,14 @@ class Block1D(nn.Module):
 
 
 class DepthwiseStem1D(nn.Module):
-    def __init__(self, C0, C1):
+    def __init__(self, C0, C1, impl="oriented"):
         super().__init__()
         self.pw_in = nn.Conv2d(3, C0, 1)
-        self.dw1 = Oriented1dDWConv(C0, 5, angles_deg=[0.0] * C0, stride=2)
-        self.dw2 = Oriented1dDWConv(C0, 5, angles_deg=[90.0] * C0)
+        self.dw1 = make_dw(C0, 5, angles=[0.0] * C0, stride=2, impl=impl)
+        self.dw2 = make_dw(C0, 5, angles=[90.0] * C0, impl=impl)
         self.pw_mid = nn.Conv2d(C0, C0, 1)
-        self.dw3 = Oriented1dDWConv(C0, 5, angles_deg=[90.0] * C0, stride=2)
-        self.dw4 = Oriented1dDWConv(C0, 5, angles_deg=[0.0] * C0)
+        self.dw3 = make_dw(C0, 5, angles=[90.0] * C0, stride=2, impl=impl)
+        self.dw4 = make_dw(C0, 5, angles=[0.0] * C0, impl=impl)
         self.pw_out = nn.Conv2d(C0, C1, 1)
         self.norm = LayerNorm2d(C1)
 
@@ -80,18 +91,18 @@ class DepthwiseStem1D(nn.Module):
 
 
 class ConvNeXt1D(nn.Module):
-    def __init__(self, name="convnext_t_1d", num_classes=1000, D=8, C0=64):
+    def __init__(self, name="convnext_t_1d", num_classes=1000, D=8, C0=64, impl="oriented"):
         super().__init__()
         cfg = CONFIGS[name]
         dims, depths = cfg["dims"], cfg["depths"]
-        self.stem = DepthwiseStem1D(C0, dims[0])
+        self.stem = DepthwiseStem1D(C0, dims[0], impl=impl)
         self.stages = nn.ModuleList()
         self.downs = nn.ModuleList()
         layer = 0
         for i, (C, n) in enumerate(zip(dims, depths)):
             blocks = []
             for _ in range(n):
-                blocks.append(Block1D(C, STAGE_K[i], D, 90.0 if layer % 2 else 0.0))
+                blocks.append(Block1D(C, STAGE_K[i], D, 90.0 if layer % 2 else 0.0, impl=impl))
                 layer += 1
             self.stages.append(nn.Sequential(*blocks))
             if i < 3:
