@@ -544,3 +544,54 @@ def test_outputs_fully_written(shape, dtype):
     B.backward_weight(plan, x, dy, dW, ws)
     torch.cuda.synchronize()
     assert torch.isfinite(y.float()).all() and torch.isfinite(dx.float()).all() and torch.isfinite(dW).all()
+
+
+@pytest.mark.parametrize("HW,K,stride", [((56, 56), 31, 1), ((14, 14), 27, 1), ((7, 7), 15, 1), ((28, 28), 31, 1),
+                                         ((30, 30), 5, 2)])
+def test_block1d_parity_vs_masked_conv2d(HW, K, stride):
+    """A ConvNeXt-1D block (oriented dw -> LN -> pw 4C -> GELU -> pw -> layer scale -> residual,
+    P:1386) through liboriented1d vs the same block with the dw layer as torch's f64 conv2d with
+    the masked KxK kernel built from the oracle's exact taps (the oracle's own pin):
+    output, input gradient and every parameter gradient (incl. dW) agree."""
+    from paper_2309_15812_b200 import convnext1d
+    torch.manual_seed(0)
+    C, N = 16, 3
+    blk = convnext1d.Block1D(C, K, 8, 90.0).cuda()
+    if stride != 1:  # the stem's strided layer inside the same block structure
+        blk.dw = convnext1d.make_dw(C, K, angles=list(B.direction_angles(8, C, "cycled")), stride=stride)
+        blk = blk.cuda()
+    blk.gamma.data.fill_(0.5)
+    x = torch.randn(N, C, *HW, device="cuda:0", requires_grad=True)
+    out = blk(x) if stride == 1 else blk.pw2(torch.nn.functional.gelu(blk.pw1(blk.norm(blk.dw(x).permute(0, 2, 3, 1)))))
+    g = torch.randn_like(out)
+    (out * g).sum().backward()
+    # reference: f64, masked KxK conv2d with the exact taps
+    ang = blk.dw.angles_deg
+    oh, ow = T.taps_table(K, K // 2, list(ang))
+    Wm = torch.zeros(C, 1, K, K, dtype=torch.float64)
+    wd = blk.dw.weight.detach().double().cpu()
+    for c in range(C):
+        for k in range(K):
+            Wm[c, 0, K // 2 + oh[c][k], K // 2 + ow[c][k]] += wd[c, k]
+    Wm = Wm.cuda().requires_grad_(True)
+    xr = x.detach().double().requires_grad_(True)
+    ref = {n: p.detach().double().clone().requires_grad_(True) for n, p in blk.named_parameters() if not n.startswith("dw")}
+    y = torch.nn.functional.conv2d(xr, Wm, stride=stride, padding=K // 2, groups=C).permute(0, 2, 3, 1)
+    y = torch.nn.functional.layer_norm(y, (C,), ref["norm.weight"], ref["norm.bias"], 1e-6)
+    y = torch.nn.functional.linear(torch.nn.functional.gelu(torch.nn.functional.linear(y, ref["pw1.weight"], ref["pw1.bias"])),
+                                   ref["pw2.weight"], ref["pw2.bias"])
+    outr = xr + (ref["gamma"] * y).permute(0, 3, 1, 2) if stride == 1 else y
+    (outr * g.double()).sum().backward()
+
+    def rel(a, b):
+        return float((a.double() - b).abs().max() / max(float(b.abs().max()), 1e-30))
+    assert rel(out, outr) <= 1e-4
+    assert rel(x.grad, xr.grad) <= 1e-4
+    dWr = torch.stack([torch.stack([Wm.grad[c, 0, K // 2 + oh[c][k], K // 2 + ow[c][k]] for k in range(K)]) for c in range(C)])
+    assert rel(blk.dw.weight.grad, dWr) <= 1e-4
+    for n, p in blk.named_parameters():
+        if not n.startswith("dw"):
+            if p.grad is None:  # (the strided variant has no residual / layer scale)
+                assert ref[n].grad is None, n
+                continue
+            assert rel(p.grad, ref[n].grad) <= 1e-4, n
