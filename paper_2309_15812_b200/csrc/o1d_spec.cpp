@@ -268,7 +268,6 @@ struct Mod {
 struct Lay {
     int P = 1, NB = 2, NS = 2, NPROD = 1, wpg = 1;
     bool early = true;  // stencil outputs stored to the staging band row by row inside the tap code
-    int pairmap = 0;    // 0: a pair's warps on one SM sub-partition; 1: on two (pairs interleaved)
     int pitch = 0, zrows = 0, hin = 0;    // ring 1: x (passes 0, 2, 3) or dy (pass 1)
     int pitch2 = 0, zrows2 = 0, hin2 = 0; // ring 2 (fused): dy with the negated tables' halo
     int dyp = 0, dyrows = 0;              // backward_weight: dense dy box per pair
@@ -1088,11 +1087,7 @@ void emit_consumer_prologue(std::ostringstream &os, const Ctx &x, const Lay &L, 
         if (fused) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
         os << "  asm volatile(\"bar.sync 1, " << nc << ";\" ::: \"memory\");\n";
     }
-    if (L.pairmap && L.wpg == 2)  // warp wg of pair q sits next to warp 1-wg of pair q-1 (SM sub-partition = warp % 4)
-        os << "  const int cw = warp - " << L.NPROD << ", wg = cw / " << L.P << ", q = (cw - wg * " << L.P << " + wg) % " << L.P << ";\n";
-    else
-        os << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n";
-    os
+    os << "  const int cw = warp - " << L.NPROD << ", q = cw % " << L.P << ", wg = cw / " << L.P << ";\n"
        << "  int bc = lane & 7, br = (lane >> 3) + 4 * wg;\n"
        << "  const bool active = bc < " << x.BC << " && br < " << x.BR << ";\n"
        << "  if (!active) { bc = 0; br = 0; }\n"
@@ -2203,7 +2198,6 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
     const int P_req = env_int("O1D_P", 0), NB_req = env_int("O1D_NBUF", 0);
     const int P3_req = env_int("O1D_P3", 0);
     const bool early = env_int("O1D_EARLY", 1) != 0;
-    const int pairmap = env_int("O1D_PAIRMAP", 0);
     bool any = false;
     for (int i = 0; i < kPasses; ++i) {
         if ((i >= 2) && d.K > 32) continue;  // per-tap reduction over one warp (v[k], k < 32)
@@ -2211,7 +2205,6 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
                               i == 3 ? P3_req : P_req, NB_req) &&
                      sp->lay[i].NB >= 2;
         sp->lay[i].early = early;
-        sp->lay[i].pairmap = pairmap;
         any = any || sp->has[i];
     }
     if (!any) return false;
