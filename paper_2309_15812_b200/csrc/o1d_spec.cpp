@@ -2452,6 +2452,57 @@ struct alignas(64) HostParams {
     void *dst;
 };
 
+// tensor maps / pointers of a small-plane launch: planes as rows of H*W elements, one box = the 32
+// samples of one channel (TMA paths); raw pointers for the cp.async paths
+static o1d_status small_maps(const o1d_plan *pl, int pass, const RunArgs &a, HostParams *hp) {
+    const SpecSet *sp = pl->spec;
+    const o1d_desc &d = pl->d;
+    hp->src1 = pass == 1 ? a.dy : a.x;
+    hp->src2 = a.dy;
+    hp->dst = pass == 0 ? a.y : a.dx;
+    if (sp->sl[pass].tma_out) {
+        const int hwo = pass == 0 ? pl->P * pl->Q : d.H * d.W;
+        if (o1d_status st = encode(&hp->out_map, hp->dst, d.dtype, hwo, 1, d.C, d.N, hwo, 1, 32)) return st;
+    }
+    if (sp->sl[pass].tma) {
+        const int hwi = pass == 1 ? pl->P * pl->Q : d.H * d.W;
+        if (o1d_status st = encode(&hp->in_map, hp->src1, d.dtype, hwi, 1, d.C, d.N, hwi, 1, 32)) return st;
+        if (pass == 2)
+            if (o1d_status st = encode(&hp->aux_map, a.dy, d.dtype, pl->P * pl->Q, 1, d.C, d.N, pl->P * pl->Q, 1, 32))
+                return st;
+    }
+    return O1D_OK;
+}
+
+// tensor maps of a spec-v2 launch: ring-1 planes x (passes 0, 2, 3) or dy (pass 1), the output band
+// (stencil) or dense dy box (backward_weight), ring-2 dy planes (fused)
+static o1d_status ring_maps(const o1d_plan *pl, int pass, const RunArgs &a, HostParams *hp) {
+    const SpecSet *sp = pl->spec;
+    const o1d_desc &d = pl->d;
+    const Lay &L = sp->lay[pass];
+    const void *in = pass == 1 ? a.dy : a.x;
+    const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
+    const bool cvt = d.dtype != O1D_F32;  // 16-bit rings are widened by the producers
+    if (L.staged) {  // raw 16-bit plane, dense box (widened by the producer from its staging buffer)
+        if (o1d_status st = encode(&hp->in_map, in, d.dtype, inW, inH, d.C, d.N, inW, L.hin)) return st;
+    } else if (cvt) {
+        hp->cvt1 = in;
+        hp->cvt2 = a.dy;
+    } else if (o1d_status st = encode(&hp->in_map, in, d.dtype, inW, inH, d.C, d.N, L.pitch, L.hin)) {
+        return st;
+    }
+    if (pass == 0 || pass == 1 || pass == 3) {  // dense output band box for the TMA store
+        void *out = pass == 0 ? a.y : a.dx;
+        const int oW = pass == 0 ? pl->Q : d.W, oH = pass == 0 ? pl->P : d.H;
+        if (o1d_status st = encode(&hp->out_map, out, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
+    }
+    if (pass == 2)  // dy plane, rows padded to whole 7-row blocks (zero-filled)
+        if (o1d_status st = encode(&hp->out_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.dyp, L.dyrows)) return st;
+    if (pass == 3 && !cvt)  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
+        if (o1d_status st = encode(&hp->aux_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.pitch2, L.hin2)) return st;
+    return O1D_OK;
+}
+
 o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream, int n0, int nlen, bool finalize,
                     bool nowait) {
     if (nlen > 0 && !spec_window_ok(pl)) return fail(O1D_UNSUPPORTED, "batch windows need the specialised kernels");
@@ -2459,49 +2510,9 @@ o1d_status spec_run(const o1d_plan *pl, int pass, const RunArgs &a, void *stream
         if (o1d_status st = ensure_fused(pl)) return st;
     const SpecSet *sp = pl->spec;
     const o1d_desc &d = pl->d;
-    const Lay &L = sp->lay[pass];
     HostParams hp;
     std::memset(&hp, 0, sizeof hp);
-    if (sp->small) {
-        hp.src1 = pass == 1 ? a.dy : a.x;
-        hp.src2 = a.dy;
-        hp.dst = pass == 0 ? a.y : a.dx;
-        if (sp->sl[pass].tma_out) {
-            const int hwo = pass == 0 ? pl->P * pl->Q : d.H * d.W;
-            if (o1d_status st = encode(&hp.out_map, hp.dst, d.dtype, hwo, 1, d.C, d.N, hwo, 1, 32)) return st;
-        }
-        if (sp->sl[pass].tma) {  // planes as rows of H*W elements: one box = 32 samples of one channel
-            const int hwi = pass == 1 ? pl->P * pl->Q : d.H * d.W;
-            if (o1d_status st = encode(&hp.in_map, hp.src1, d.dtype, hwi, 1, d.C, d.N, hwi, 1, 32)) return st;
-            if (pass == 2)
-                if (o1d_status st = encode(&hp.aux_map, a.dy, d.dtype, pl->P * pl->Q, 1, d.C, d.N, pl->P * pl->Q, 1, 32))
-                    return st;
-        }
-    } else {
-    // ring-1 planes: x (passes 0, 2, 3) or dy (pass 1), box = image rows x pitch columns
-    const void *in = pass == 1 ? a.dy : a.x;
-    const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
-    const bool cvt = d.dtype != O1D_F32;  // 16-bit rings are widened by the producers (no TMA map)
-    if (L.staged) {  // raw 16-bit plane, dense box (widened by the producer from its staging buffer)
-        if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, inW, L.hin)) return st;
-    } else if (cvt) {
-        hp.cvt1 = in;
-        hp.cvt2 = a.dy;
-    } else if (o1d_status st = encode(&hp.in_map, in, d.dtype, inW, inH, d.C, d.N, L.pitch, L.hin)) {
-        return st;
-    }
-    if (pass == 0 || pass == 1 || pass == 3) {  // dense output band box for the TMA store
-        void *out = pass == 0 ? a.y : a.dx;
-        const int oW = pass == 0 ? pl->Q : d.W, oH = pass == 0 ? pl->P : d.H;
-        if (o1d_status st = encode(&hp.out_map, out, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
-    }
-    if (pass == 2) {  // dy plane, rows padded to whole 7-row blocks (zero-filled)
-        if (o1d_status st = encode(&hp.out_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.dyp, L.dyrows)) return st;
-    }
-    if (pass == 3 && !cvt) {  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
-        if (o1d_status st = encode(&hp.aux_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.pitch2, L.hin2)) return st;
-    }
-    }
+    if (o1d_status st = sp->small ? small_maps(pl, pass, a, &hp) : ring_maps(pl, pass, a, &hp)) return st;
     hp.w = a.w;
     hp.ws = a.ws;
     hp.dW = a.dW;
