@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <functional>
 #include <string>
 
 #include "o1d_internal.h"
@@ -35,6 +37,24 @@ template <> __device__ __forceinline__ __half to_act<__half>(float v) { return _
 
 constexpr int kThreads = 256;
 constexpr int kSmemBudget = 96 * 1024;
+// preferred shared memory per CTA when choosing a band height: small enough for several CTAs per
+// SM, so the staging loads of one CTA overlap the compute of the others (O1D_GENERIC_KB)
+size_t pref_budget() {
+    static const size_t kb = [] {
+        const char *v = getenv("O1D_GENERIC_KB");
+        const int k = (v && *v) ? atoi(v) : 48;
+        return (size_t)std::max(4, std::min(96, k)) * 1024;
+    }();
+    return kb;
+}
+int pick_band(int rows, const std::function<size_t(int)> &smem_for) {
+    int band = rows;
+    while (band > 1 && smem_for(band) > pref_budget()) band = (band + 1) / 2;
+    if (smem_for(band) <= pref_budget()) return band;
+    band = rows;
+    while (band > 1 && smem_for(band) > (size_t)kSmemBudget) band = (band + 1) / 2;
+    return smem_for(band) <= (size_t)kSmemBudget ? band : 0;
+}
 
 // tile[r][j] = plane[h0 + r][v0 + j] as fp32 (zero outside the Hi x Wi image, reading R1), r < rows,
 // j < cols.  Image rows whose byte length is a multiple of 16 are read in 16-byte vectors (the
@@ -272,11 +292,12 @@ struct BwdWArgs {
     int tileRows, tileCols, pitch;
 };
 
-// Reduce 32 per-lane values so that lane L ends with sum over lanes of v[L] (31 shuffles).
-__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
+// NV per-lane values -> lane L (< NV) ends with the warp sum of v[L] (NV a power of two <= 32)
+template <int NV>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[NV]) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
+    for (int s = NV / 2; s >= 1; s >>= 1) {
         const bool upper = lane & s;
 #pragma unroll
         for (int i = 0; i < s; ++i) {
@@ -285,11 +306,15 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
     }
-    return v[0];
+    float r = v[0];
+#pragma unroll
+    for (int s = NV; s < 32; s <<= 1) r += __shfl_xor_sync(0xffffffffu, r, s);
+    return r;
 }
 
-// ws[plane*bands + band][e] = sum over the band's outputs of dy[p][q] * x[str*p+oh_e][str*q+ow_e] (expanded taps)
-template <typename T>
+// ws[plane*bands + band][e] = sum over the band's outputs of dy[p][q] * x[str*p+oh_e][str*q+ow_e] (expanded taps);
+// KC taps per round (8 for short kernels such as the stem's K=5, else 32)
+template <typename T, int KC>
 __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a) {
     extern __shared__ float sm[];
     __shared__ float red[kThreads / 32][32];
@@ -312,20 +337,20 @@ __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a
     stage_tile<T>(sdy, a.Q, dy - (size_t)p0 * a.Q, a.P, a.Q, p0, nrows, 0, a.Q);
     __syncthreads();
     float *ws = a.ws + (size_t)blockIdx.x * a.K;
-    for (int k0 = 0; k0 < a.K; k0 += 32) {
-        float acc[32];
+    for (int k0 = 0; k0 < a.K; k0 += KC) {
+        float acc[KC];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        const int kn = min(32, a.K - k0);
+        for (int j = 0; j < KC; ++j) acc[j] = 0.f;
+        const int kn = min(KC, a.K - k0);
         for (int g = tid; g < nrows * a.Q; g += blockDim.x) {
             const int pr = g / a.Q, q = g - pr * a.Q;
             const float gv = sdy[g];
             const float *base = tile + pr * a.str * a.pitch + q * a.str;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < KC; ++j)
                 if (j < kn) acc[j] = fmaf(gv, base[toff[k0 + j]], acc[j]);
         }
-        const float r = warp_reduce_scatter32(acc);
+        const float r = warp_reduce_scatter<KC>(acc);
         red[warp][lane] = r;
         __syncthreads();
         if (tid < 32 && tid < kn) {
@@ -402,10 +427,7 @@ size_t stencil_smem(const Stencil &st, int band, int extra_rows_per_out) {
 size_t dtype_size(int dt) { return dt == O1D_F32 ? 4 : 2; }
 
 int generic_band_rows(const o1d_plan *, const Stencil &st, int extra) {
-    int band = st.Ho;
-    while (band > 1 && stencil_smem(st, band, extra) > (size_t)kSmemBudget) band = (band + 1) / 2;
-    if (stencil_smem(st, band, extra) > (size_t)kSmemBudget) return 0;
-    return band;
+    return pick_band(st.Ho, [&](int b) { return stencil_smem(st, b, extra); });
 }
 
 o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, const void *in, const float *w,
@@ -440,11 +462,10 @@ o1d_status generic_bwd_input_strided(const o1d_plan *pl, const void *dy, const f
         const int s = d.stride;
         a.tileCols = (d.W - 1 + a.maxOW - a.minOW) / s + 2;
         a.pitch = a.tileCols + ((a.tileCols & 31) == 0 ? 1 : 0);
-        int band = d.H;
         auto rows_for = [&](int b) { return (b - 1 + a.maxOH - a.minOH) / s + 2; };
         auto smem_for = [&](int b) { return sizeof(float) * ((size_t)rows_for(b) * a.pitch + 2 * a.KE); };
-        while (band > 1 && smem_for(band) > (size_t)kSmemBudget) band = (band + 1) / 2;
-        if (smem_for(band) <= (size_t)kSmemBudget) {
+        const int band = pick_band(d.H, smem_for);
+        if (band > 0) {
             a.band = band;
             a.bands = (d.H + band - 1) / band;
             a.tileRows = rows_for(band);
@@ -488,7 +509,7 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     o1d_status r = dispatch_dtype(d.dtype, [&](auto tag) -> o1d_status {
         using T = decltype(tag);
-        auto kern = bwd_weight_generic_kernel<T>;
+        auto kern = a.K <= 8 ? bwd_weight_generic_kernel<T, 8> : bwd_weight_generic_kernel<T, 32>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return check_launch("bwd_weight_generic attr");
         kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
