@@ -152,7 +152,9 @@ struct StencilArgs {
 };
 
 // out[p][q] = sum_e in[str*p + dh_e][str*q + dw_e] * coef_e * w_{k_e}, one CTA per (plane, band of output rows)
-template <typename T>
+// KC > 0: at most KC expanded taps, their offsets and weights held in registers (short kernels
+// such as the stem's K=5); KC = 0: any count, read from shared memory per tap
+template <typename T, int KC>
 __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a) {
     extern __shared__ float sm[];
     const int tid = threadIdx.x;
@@ -176,17 +178,39 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     __syncthreads();
     T *out = static_cast<T *>(a.out) + (size_t)plane * a.Ho * a.Wo;
     const int qg = (a.Wo + 3) >> 2;
+    int roff[KC > 0 ? KC : 1];
+    float rw[KC > 0 ? KC : 1];
+    if constexpr (KC > 0) {
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            roff[k] = k < a.KE ? toff[k] : 0;
+            rw[k] = k < a.KE ? wk[k] : 0.f;
+        }
+    }
     for (int g = tid; g < nrows * qg; g += blockDim.x) {
         const int pr = g / qg, q0 = (g - pr * qg) * 4;
         const float *base = tile + pr * a.str * a.pitch + q0 * a.str;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-        for (int k = 0; k < a.KE; ++k) {
-            const float *s = base + toff[k];
-            const float wv = wk[k];
-            acc0 = fmaf(s[0], wv, acc0);
-            acc1 = fmaf(s[a.str], wv, acc1);
-            acc2 = fmaf(s[2 * a.str], wv, acc2);
-            acc3 = fmaf(s[3 * a.str], wv, acc3);
+        if constexpr (KC > 0) {
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                if (k >= a.KE) break;  // (no padding taps: 0 * inf would leak a non-finite input)
+                const float *s = base + roff[k];
+                const float wv = rw[k];
+                acc0 = fmaf(s[0], wv, acc0);
+                acc1 = fmaf(s[a.str], wv, acc1);
+                acc2 = fmaf(s[2 * a.str], wv, acc2);
+                acc3 = fmaf(s[3 * a.str], wv, acc3);
+            }
+        } else {
+            for (int k = 0; k < a.KE; ++k) {
+                const float *s = base + toff[k];
+                const float wv = wk[k];
+                acc0 = fmaf(s[0], wv, acc0);
+                acc1 = fmaf(s[a.str], wv, acc1);
+                acc2 = fmaf(s[2 * a.str], wv, acc2);
+                acc3 = fmaf(s[3 * a.str], wv, acc3);
+            }
         }
         const float acc[4] = {acc0, acc1, acc2, acc3};
         store4<T>(out + (size_t)(p0 + pr) * a.Wo + q0, acc, min(4, a.Wo - q0));
@@ -443,7 +467,7 @@ o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, cons
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     return dispatch_dtype(pl->d.dtype, [&](auto tag) -> o1d_status {
         using T = decltype(tag);
-        auto kern = stencil_generic_kernel<T>;
+        auto kern = a.KE <= 8 ? stencil_generic_kernel<T, 8> : stencil_generic_kernel<T, 0>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return check_launch("stencil_generic attr");
         kern<<<(unsigned)grid, kThreads, smem, s>>>(a);
