@@ -595,3 +595,26 @@ def test_block1d_parity_vs_masked_conv2d(HW, K, stride):
                 assert ref[n].grad is None, n
                 continue
             assert rel(p.grad, ref[n].grad) <= 1e-4, n
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_small_planes_repeated_bitwise(dtype):
+    """The small-plane kernels at the K-sweep shape: 40 back-to-back launches of every pass give
+    bitwise-identical results (dynamic scheduling, slot reuse, PDL overlap between launches)."""
+    N, C, H, W, K = 128, 384, 14, 14, 31
+    plan = B.Plan(N, C, H, W, K, B.direction_angles(8, C, "cycled"), dtype=dtype, device="cuda:0")
+    assert plan.describe().startswith("spec-small"), plan.describe()
+    x = torch.from_numpy(inputs.activation((N, C, H, W), 0)).to("cuda:0", dtype)
+    dy = torch.from_numpy(inputs.activation((N, C, H, W), 2)).to("cuda:0", dtype)
+    w = torch.from_numpy(inputs.weights(C, K, 1)).cuda()
+    ws = B.workspace(plan)
+    y0, dx0, dW0 = B.forward(plan, x, w), B.backward_input(plan, dy, w), B.backward_weight(plan, x, dy, ws=ws)
+    y, dx, dW = torch.empty_like(y0), torch.empty_like(dx0), torch.empty_like(dW0)
+    bad = 0
+    for _ in range(40):
+        B.forward(plan, x, w, y)
+        B.backward_input(plan, dy, w, dx)
+        B.backward_weight(plan, x, dy, dW, ws)
+        torch.cuda.synchronize()
+        bad += int(not (torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0)))
+    assert bad == 0, bad
