@@ -926,6 +926,35 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
        << "  __syncthreads();\n";
 }
 
+// Widening of one 16-bit plane (Hin rows of Win elements, dense, at `src`) into an fp32 slot (`dst`, rows
+// `pitch` floats apart) by one warp: lane -> (row wr of a group of RPI rows, 16-byte chunk wc of the row),
+// computed once per plane, then one fully unrolled LDS/LDG.128 -> 8 x widen -> 2 x STS.128 per row group
+// with immediate offsets (the chunk index division of the round-2 loop cost ~45 instructions per chunk in a
+// kernel whose SM sub-partitions are issue-bound).  All loads of the plane are in flight before the first
+// store.  The pad columns [Win, pitch) are zeroed once in the consumer prologue (never written here).
+void emit_widen(std::ostringstream &os, const std::string &src, bool global, int Hin, int Win, const std::string &dst, int pitch,
+                const char *ind) {
+    const int cpr = Win / 8, rpi = 32 / cpr, iters = (Hin + rpi - 1) / rpi;
+    os << ind << "{\n"
+       << ind << "  const int wr = lane / " << cpr << ", wc = lane - wr * " << cpr << ";\n"
+       << ind << "  if (wr < " << rpi << ") {\n"
+       << ind << "    const uint4* const s0 = reinterpret_cast<const uint4*>(" << src << ") + wr * " << cpr << " + wc;\n"
+       << ind << "    float* const d0 = " << dst << " + wr * " << pitch << " + wc * 8;\n"
+       << ind << "    uint4 v[" << iters << "];\n";
+    for (int it = 0; it < iters; ++it) {
+        const bool guard = (it + 1) * rpi > Hin;
+        os << ind << "    " << (guard ? "if (wr + " + std::to_string(it * rpi) + " < " + std::to_string(Hin) + ") " : "") << "v[" << it
+           << "] = " << (global ? "ldg_stream(s0 + " + std::to_string(it * rpi * cpr) + ", pol)" : "s0[" + std::to_string(it * rpi * cpr) + "]")
+           << ";\n";
+    }
+    for (int it = 0; it < iters; ++it) {
+        const bool guard = (it + 1) * rpi > Hin;
+        os << ind << "    " << (guard ? "if (wr + " + std::to_string(it * rpi) + " < " + std::to_string(Hin) + ") " : "") << "{ float4* d = reinterpret_cast<float4*>(d0 + "
+           << it * rpi * pitch << "); d[0] = w4(v[" << it << "].x, v[" << it << "].y); d[1] = w4(v[" << it << "].z, v[" << it << "].w); }\n";
+    }
+    os << ind << "  }\n" << ind << "}\n";
+}
+
 // Producer warps.  Pair q owns slots q*NB .. q*NB+NB-1; its j-th item goes to slot
 // q*NB + j % NB.  One producer per pair (P <= 4) sleeps in try_wait until the pair frees a
 // slot; with more pairs two producers poll theirs round-robin so a slow pair never holds up
@@ -1019,30 +1048,11 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
         // flight before the first use, widens them to fp32 and stores them into the slot's
         // image columns; the arrive below releases them to the consumers (mbarrier release)
         auto widen = [&](const char *srcp, int Hin, int Win, size_t slot_off, size_t slot_stride, int pitch) {
-            const int cpr = Win / 8, nch = Hin * cpr, nj = (nch + 31) / 32;
-            const int ppr = (pitch - Win) / 4, npad = Hin * ppr;  // zero float4s of the pad columns
-            os << "        if (item >= 0) {\n"
-               << "          const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const act_t*>(" << srcp
-               << ") + ((u64)n2 * " << x.C << " + c2) * " << (long)Hin * Win << ");\n"
-               << "          float* dst = reinterpret_cast<float*>(smem + " << slot_off << " + s * " << slot_stride << ");\n"
-               << "          uint4 v[" << nj << "];\n"
-               << "#pragma unroll\n"
-               << "          for (int j = 0; j < " << nj << "; ++j) { const int i = lane + 32 * j; if (i < " << nch
-               << ") v[j] = ldg_stream(src + i, pol); }\n"
-               << "#pragma unroll\n"
-               << "          for (int j = 0; j < " << nj << "; ++j) {\n"
-               << "            const int i = lane + 32 * j;\n"
-               << "            if (i < " << nch << ") {\n"
-               << "              const int r = i / " << cpr << ", cc = i - r * " << cpr << ";\n"
-               << "              float4* d = reinterpret_cast<float4*>(dst + r * " << pitch << " + cc * 8);\n"
-               << "              d[0] = w4(v[j].x, v[j].y); d[1] = w4(v[j].z, v[j].w);\n"
-               << "            }\n"
-               << "          }\n"
-               << "          for (int i = lane; i < " << npad << "; i += 32) {   // columns past the image: zero (reading R1)\n"
-               << "            const int r = i / " << ppr << ", cc = i - r * " << ppr << ";\n"
-               << "            *reinterpret_cast<float4*>(dst + r * " << pitch << " + " << Win << " + cc * 4) = make_float4(0.f, 0.f, 0.f, 0.f);\n"
-               << "          }\n"
-               << "        }\n";
+            os << "        if (item >= 0)\n";
+            emit_widen(os, "reinterpret_cast<const act_t*>(" + std::string(srcp) + ") + ((u64)n2 * " + std::to_string(x.C) + " + c2) * " +
+                               std::to_string((long)Hin * Win),
+                       true, Hin, Win, "reinterpret_cast<float*>(smem + " + std::to_string(slot_off) + " + s * " + std::to_string(slot_stride) + ")",
+                       pitch, "        ");
         };
         widen("p.cvt1", L.hin, pass == 1 ? x.Wo : x.Wi, L.off_t + L.zb, L.zb + L.tb, L.pitch);
         if (fused) widen("p.cvt2", L.hin2, x.Wo, L.off_t2 + L.zb2, L.zb2 + L.tb2, L.pitch2);
@@ -1076,13 +1086,18 @@ void emit_consumer_prologue(std::ostringstream &os, const Ctx &x, const Lay &L, 
     {
         const int nc = 32 * L.ncw();
         emit_zero_ring(os, L.off_t, L.zb, L.tb, (size_t)L.hin * L.pitch * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
-        if (L.staged) {  // columns [W, pitch) of every slot row: the widening producers write only [0, W)
-            const int ppr = (L.pitch - x.Wo) / 4;
-            os << "  for (int i = tid - " << 32 * L.NPROD << "; i < " << L.NS * L.hin * ppr << "; i += " << nc << ") {\n"
-               << "    const int s = i / " << L.hin * ppr << ", k = i - s * " << L.hin * ppr << ", r = k / " << ppr << ", cc = k - r * " << ppr << ";\n"
-               << "    *reinterpret_cast<float4*>(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << " + (r * " << L.pitch << " + "
-               << x.Wo << " + cc * 4) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);\n"
+        auto zero_pad = [&](size_t off, size_t zb, size_t tb, int hin, int pitch, int win) {
+            // columns [W, pitch) of every slot row: the widening producers write only [0, W)
+            const int ppr = (pitch - win) / 4;
+            os << "  for (int i = tid - " << 32 * L.NPROD << "; i < " << L.NS * hin * ppr << "; i += " << nc << ") {\n"
+               << "    const int s = i / " << hin * ppr << ", k = i - s * " << hin * ppr << ", r = k / " << ppr << ", cc = k - r * " << ppr << ";\n"
+               << "    *reinterpret_cast<float4*>(smem + " << off + zb << " + s * " << zb + tb << " + (r * " << pitch << " + "
+               << win << " + cc * 4) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);\n"
                << "  }\n";
+        };
+        if (x.act != O1D_F32) {  // 16-bit planes are widened into the fp32 rings (staged or per lane)
+            zero_pad(L.off_t, L.zb, L.tb, L.hin, L.pitch, pass == 0 || pass == 2 || fused ? x.Wi : x.Wo);
+            if (fused) zero_pad(L.off_t2, L.zb2, L.tb2, L.hin2, L.pitch2, x.Wo);
         }
         if (fused) emit_zero_ring(os, L.off_t2, L.zb2, L.tb2, (size_t)L.hin2 * L.pitch2 * 4, L.NS, nc, "(tid - " + std::to_string(32 * L.NPROD) + ")");
         os << "  asm volatile(\"bar.sync 1, " << nc << ";\" ::: \"memory\");\n";
@@ -1104,7 +1119,7 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
     const bool wgrad = pass == 2;
     const int Win = x.Wo;  // stride 1: input width = output width
     const size_t raw = (size_t)L.hin * Win * es;
-    const int cpr = Win * es / 16, nch = L.hin * cpr;
+    (void)es;
     const int PREF = 2;
     auto claim = [&](const char *var) {
         os << "      {\n"
@@ -1171,19 +1186,9 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
     os << "      }\n"
        << "      if (item >= 0) {\n"
        << "        mbar_wait(stfull, j & 1);\n"
-       << "        float* const dst = reinterpret_cast<float*>(smem + " << L.off_t + L.zb << " + s * " << L.zb + L.tb << ");\n"
-       << "#pragma unroll 4\n"
-       << "        for (int i = lane; i < " << nch << "; i += 32) {\n"
-       << "          const uint4 v = *reinterpret_cast<const uint4*>(stage + i * 16);\n"
-       << "          const int r = i / " << cpr << ", cc = i - r * " << cpr << ";\n"
-       << "          float4* d = reinterpret_cast<float4*>(dst + r * " << L.pitch << " + cc * 8);\n"
-       // the two 16-byte halves in a lane-dependent order: eight consecutive lanes (chunks 32 B
-       // apart) then hit eight distinct 16-byte bank groups in each store instruction
-       << "          const float4 lo4 = w4(v.x, v.y), hi4 = w4(v.z, v.w);\n"
-       << "          const bool sw = (i >> 2) & 1;\n"
-       << "          d[sw] = sw ? hi4 : lo4;\n"
-       << "          d[!sw] = sw ? lo4 : hi4;\n"
-       << "        }\n";
+       ;
+    emit_widen(os, "stage", false, L.hin, Win, "reinterpret_cast<float*>(smem + " + std::to_string(L.off_t + L.zb) + " + s * " + std::to_string(L.zb + L.tb) + ")",
+               L.pitch, "        ");
     if (!wgrad)
         os << "        for (int k = lane; k < " << x.K << "; k += 32) wsm[s * 64 + k] = __ldg(p.w + c2 * " << x.K << " + k);\n";
     os << "      }\n"
