@@ -277,6 +277,10 @@ struct Lay {
     // widened to the fp32 slot by the pair's producer (else: per-lane 16-byte loads, see emit_producer)
     bool staged = false;
     size_t stb = 0, off_st = 0;
+    // 16-bit planes whose rows are not 16-byte multiples (ConvNeXt stage 2: 28 x 2 B): every TMA box views
+    // a plane as rows of 8 elements (the plane itself is a 16-byte multiple), so only dense whole-row boxes
+    // are used (raw input plane, dy block, output band) and the widening maps elements to (row, column)
+    bool flat = false;
     int ncw() const { return P * wpg; }
     size_t ring1() const { return zb + (size_t)NS * (zb + tb); }
     size_t ring2() const { return tb2 ? zb2 + (size_t)NS * (zb2 + tb2) : 0; }
@@ -469,6 +473,7 @@ struct Ctx {
     int C, K, Ho, Wo, BR, BC, nt, nsm;
     int Wi = 0;                    // input width (x)
     int act = 0;                   // activation dtype (o1d_dtype)
+    bool flat = false;             // planes viewed as rows of 8 elements by the TMA maps (Lay::flat)
     std::vector<int> home;         // home table per %smid (empty: TPC-pair fallback)
     std::vector<int> table_of;
 };
@@ -841,10 +846,12 @@ bool make_lay(Lay *Lp, int pass, int wpg, const std::vector<Geo> &fwd, const std
         ring_geom(bwd, Ho, BR, 4, &L.pitch2, &L.zrows2, &L.zb2, &L.tb2);
         L.hin2 = Ho;
     }
+    L.flat = (Wo * es) % 16 != 0;
     if (wgrad) {
         const int vec = 16 / es;
-        L.dyp = (S * BC + vec - 1) & ~(vec - 1);
+        L.dyp = L.flat ? Wo : (S * BC + vec - 1) & ~(vec - 1);
         L.dyrows = R * BR;
+        while (L.flat && (L.dyrows * Wo) % 8 != 0) ++L.dyrows;  // whole 8-element rows of the flat view (zero-filled past P)
         L.db = ((size_t)L.dyp * L.dyrows * es + 127) & ~(size_t)127;
     }
     const size_t budget = (size_t)227 * 1024 - 64;
@@ -855,7 +862,8 @@ bool make_lay(Lay *Lp, int pass, int wpg, const std::vector<Geo> &fwd, const std
     auto fit = [&](int P, int NB) {
         L.P = P, L.NB = NB, L.NS = P * NB;
         if (L.NS > NSmax || P * wpg > 15) return false;
-        L.NPROD = P <= 4 ? P : 2;
+        // more than 4 pairs: 2 producers poll theirs round-robin (4 when they widen 16-bit planes)
+        L.NPROD = P <= 4 ? P : es != 4 ? 4 : 2;
         // header: full[16], empty[16], dyempty[8] mbarriers | s_item[16] | weights | bands | dy slots | rings
         L.off_item = 8 * (2 * (size_t)NSmax + 16);  // + stfull[8]
         L.off_w = (L.off_item + 4 * (size_t)NSmax + 15) & ~(size_t)15;
@@ -934,6 +942,27 @@ void emit_prologue(std::ostringstream &os, const Lay &L, int pass, int es) {
 // store.  The pad columns [Win, pitch) are zeroed once in the consumer prologue (never written here).
 void emit_widen(std::ostringstream &os, const std::string &src, bool global, int Hin, int Win, const std::string &dst, int pitch,
                 const char *ind) {
+    if (Win % 8 != 0) {
+        // rows of 4-element units that straddle 16-byte chunks (flat planes, Lay::flat): chunk k holds
+        // elements 8k .. 8k+7, each half (4 elements) lies in one row
+        const int nch = Hin * Win / 8, iters = (nch + 31) / 32;
+        os << ind << "{\n"
+           << ind << "  const uint4* const s0 = reinterpret_cast<const uint4*>(" << src << ") + lane;\n"
+           << ind << "  float* const d0 = " << dst << ";\n"
+           << ind << "  uint4 v[" << iters << "];\n";
+        for (int it = 0; it < iters; ++it)
+            os << ind << "  if (lane + " << 32 * it << " < " << nch << ") v[" << it << "] = "
+               << (global ? "ldg_stream(s0 + " + std::to_string(32 * it) + ", pol)" : "s0[" + std::to_string(32 * it) + "]") << ";\n";
+        for (int it = 0; it < iters; ++it)
+            os << ind << "  if (lane + " << 32 * it << " < " << nch << ") {\n"
+               << ind << "    const int e0 = 8 * (lane + " << 32 * it << "), r0 = e0 / " << Win << ", c0 = e0 - r0 * " << Win << ";\n"
+               << ind << "    const int e1 = e0 + 4, r1 = e1 / " << Win << ", c1 = e1 - r1 * " << Win << ";\n"
+               << ind << "    *reinterpret_cast<float4*>(d0 + r0 * " << pitch << " + c0) = w4(v[" << it << "].x, v[" << it << "].y);\n"
+               << ind << "    *reinterpret_cast<float4*>(d0 + r1 * " << pitch << " + c1) = w4(v[" << it << "].z, v[" << it << "].w);\n"
+               << ind << "  }\n";
+        os << ind << "}\n";
+        return;
+    }
     const int cpr = Win / 8, rpi = 32 / cpr, iters = (Hin + rpi - 1) / rpi;
     os << ind << "{\n"
        << ind << "  const int wr = lane / " << cpr << ", wc = lane - wr * " << cpr << ";\n"
@@ -1233,7 +1262,8 @@ void emit_band_head(std::ostringstream &os, const Ctx &x, const char *ind) {
 void emit_band_tail(std::ostringstream &os, const Ctx &x, const char *ind) {
     os << ind << "asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
        << ind << "__syncwarp();\n"
-       << ind << "if (lane == 0 && row0 < " << x.Ho << ") tma_store_band(&p.out_map, stg, row0, c, n, policy_evict_first());\n";
+       << ind << "if (lane == 0 && row0 < " << x.Ho << ") tma_store_band(&p.out_map, stg, " << (x.flat ? "row0 * " + std::to_string(x.Wo / 2) + " / 4" : "row0")
+       << ", c, n, policy_evict_first());\n";
 }
 
 // stencil outputs: registers -> this warp's staging band -> TMA bulk store (evict-first)
@@ -1252,7 +1282,8 @@ void emit_band_store(std::ostringstream &os, const Ctx &x, const Lay &L) {
     os << "    }\n"
        << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
        << "    __syncwarp();\n"
-       << "    if (lane == 0 && row0 < " << x.Ho << ") tma_store_band(&p.out_map, stg, row0, c, n, policy_evict_first());\n";
+       << "    if (lane == 0 && row0 < " << x.Ho << ") tma_store_band(&p.out_map, stg, " << (x.flat ? "row0 * " + std::to_string(x.Wo / 2) + " / 4" : "row0")
+       << ", c, n, policy_evict_first());\n";
 }
 
 void emit_wgrad_write(std::ostringstream &os, const Ctx &x, const Lay &L, int NV) {
@@ -1411,7 +1442,10 @@ std::string gen_pass(const Ctx &x, const Lay &L, int pass, const Cases &st, cons
     } else if (pass == 2) {
         for (int r = 0; r < R; ++r)
             for (int s = 0; s < S; ++s)
-                os << "    const float g" << r << "_" << s << " = active ? LD(dys[" << r * L.dyp + s << "]) : 0.f;\n";
+                os << "    const float g" << r << "_" << s << " = active"
+                   // flat dy rows are dense: columns past the plane (ragged last block) belong to the next row
+                   << (L.flat && S * x.BC > x.Wo ? " && " + std::to_string(S) + " * bc + " + std::to_string(s) + " < " + std::to_string(x.Wo) : std::string())
+                   << " ? LD(dys[" << r * L.dyp + s << "]) : 0.f;\n";
         os << "    __syncwarp();\n"
            << "    if (lane == 0) mbar_arrive(dyempty + q);   // dy block in registers: the pair's dy slot is free\n"
            << "    float v[" << NV << "];   // v[k], k < K: assigned by the table's case\n"
@@ -2172,7 +2206,12 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
     if (d.K > 64 || pl->n_distinct > 16) return false;
     if (d.H <= 2 * R && d.W <= 2 * S && env_int("O1D_SMALL", 1) != 0)
         return small_prepare(pl, sp, src, nsm, gpc);
-    if ((d.W * es) % 16 != 0) return false;
+    if ((d.W * es) % 16 != 0) {
+        // 16-bit rows that are not 16-byte multiples: flat TMA views (Lay::flat) need whole planes of
+        // 16-byte multiples, rows of 4-element (8-byte) units, band starts on 8-element boundaries
+        // (28-row bands, W even) and boxes of <= 256 eight-element rows
+        if (es != 2 || d.W % 4 != 0 || ((long)d.H * d.W) % 8 != 0 || (long)d.H * d.W / 8 > 256) return false;
+    }
     if (pl->n_distinct > 16 || (long)d.N * d.C >= (1L << 22)) return false;
     if (d.W > 256 || d.H > 256) return false;
     sp->BR = (pl->P + R - 1) / R;
@@ -2220,6 +2259,7 @@ bool spec_prepare(const o1d_plan *pl, SpecSet *sp, std::string src[kPasses], int
                                                           L.early ? &x : nullptr);
         const Cases wg = i >= 2 ? wgrad_cases(sp->fwd, L.pitch, d.K) : Cases{};
         Ctx xi = x;
+        xi.flat = L.flat;
         if (gpc && !gpc->empty()) {
             // SMs per table in proportion to planes x the issue count of the table's case(s) in
             // THIS pass (+100: per-item cost outside the case; the wgrad's per-table costs differ
@@ -2489,7 +2529,9 @@ static o1d_status ring_maps(const o1d_plan *pl, int pass, const RunArgs &a, Host
     const int inW = pass == 1 ? pl->Q : d.W, inH = pass == 1 ? pl->P : d.H;
     const bool cvt = d.dtype != O1D_F32;  // 16-bit rings are widened by the producers
     if (L.staged) {  // raw 16-bit plane, dense box (widened by the producer from its staging buffer)
-        if (o1d_status st = encode(&hp->in_map, in, d.dtype, inW, inH, d.C, d.N, inW, L.hin)) return st;
+        if (o1d_status st = L.flat ? encode(&hp->in_map, in, d.dtype, 8, inH * inW / 8, d.C, d.N, 8, L.hin * inW / 8)
+                                   : encode(&hp->in_map, in, d.dtype, inW, inH, d.C, d.N, inW, L.hin))
+            return st;
     } else if (cvt) {
         hp->cvt1 = in;
         hp->cvt2 = a.dy;
@@ -2499,10 +2541,14 @@ static o1d_status ring_maps(const o1d_plan *pl, int pass, const RunArgs &a, Host
     if (pass == 0 || pass == 1 || pass == 3) {  // dense output band box for the TMA store
         void *out = pass == 0 ? a.y : a.dx;
         const int oW = pass == 0 ? pl->Q : d.W, oH = pass == 0 ? pl->P : d.H;
-        if (o1d_status st = encode(&hp->out_map, out, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R))) return st;
+        if (o1d_status st = L.flat ? encode(&hp->out_map, out, d.dtype, 8, oH * oW / 8, d.C, d.N, 8, std::min(oH, 4 * R) * oW / 8)
+                                   : encode(&hp->out_map, out, d.dtype, oW, oH, d.C, d.N, oW, std::min(oH, 4 * R)))
+            return st;
     }
     if (pass == 2)  // dy plane, rows padded to whole 7-row blocks (zero-filled)
-        if (o1d_status st = encode(&hp->out_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.dyp, L.dyrows)) return st;
+        if (o1d_status st = L.flat ? encode(&hp->out_map, a.dy, d.dtype, 8, pl->P * pl->Q / 8, d.C, d.N, 8, L.dyrows * pl->Q / 8)
+                                   : encode(&hp->out_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.dyp, L.dyrows))
+            return st;
     if (pass == 3 && !cvt)  // dy planes for ring 2 (the dx stencil's input, the dy block of the partials)
         if (o1d_status st = encode(&hp->aux_map, a.dy, d.dtype, pl->Q, pl->P, d.C, d.N, L.pitch2, L.hin2)) return st;
     return O1D_OK;

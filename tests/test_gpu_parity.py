@@ -618,3 +618,15 @@ def test_small_planes_repeated_bitwise(dtype):
         torch.cuda.synchronize()
         bad += int(not (torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0)))
     assert bad == 0, bad
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("shape", [(4, 16, 28, 28, 31, "cycled"), (3, 8, 36, 28, 15, "contiguous"),
+                                   (2, 8, 20, 44, 31, "cycled"), (5, 16, 28, 28, 7, "contiguous")])
+def test_flat_16bit_planes(shape, dtype):
+    """16-bit planes whose rows are not 16-byte multiples (ConvNeXt stage 2: 28 x 2 B) on the specialised
+    kernels through flat TMA views (planes as rows of 8 elements) and the element-to-(row, column) widening."""
+    N, C, H, W, K, assign = shape
+    angles = B.direction_angles(8, C, assign)
+    plan, errs = run_case(N, C, H, W, K, angles, dtype=dtype, check_det=True, expect="spec")
+    assert "spec-small" not in plan.describe()
