@@ -57,17 +57,19 @@ int pick_band(int rows, const std::function<size_t(int)> &smem_for) {
 }
 
 // tile[r][j] = plane[h0 + r][v0 + j] as fp32 (zero outside the Hi x Wi image, reading R1), r < rows,
-// j < cols.  Image rows whose byte length is a multiple of 16 are read in 16-byte vectors (the
-// activations may be 2-byte bf16/fp16: one vector load instead of eight scalar ones).
+// j < cols; only rows r that are multiples of rstep (the rows the taps read, Stencil::rstep).  Image
+// rows whose byte length is a multiple of 16 are read in 16-byte vectors (the activations may be
+// 2-byte bf16/fp16: one vector load instead of eight scalar ones).
 template <typename T>
 __device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plane, int Hi, int Wi, int h0, int rows,
-                                           int v0, int cols) {
+                                           int v0, int cols, int rstep = 1) {
     const int tid = threadIdx.x, nt = blockDim.x;
     constexpr int V = 16 / sizeof(T);
     const bool vec = ((Wi * (int)sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(plane) & 15) == 0);
+    const int nr = (rows + rstep - 1) / rstep;  // staged rows: r = k * rstep, k < nr
     if (!vec) {
-        for (int i = tid; i < rows * cols; i += nt) {
-            const int r = i / cols, j = i - r * cols;
+        for (int i = tid; i < nr * cols; i += nt) {
+            const int k = i / cols, j = i - k * cols, r = k * rstep;
             const int h = h0 + r, v = v0 + j;
             tile[r * pitch + j] = (h >= 0 && h < Hi && v >= 0 && v < Wi) ? ld_act<T>(plane + (size_t)h * Wi + v) : 0.f;
         }
@@ -75,27 +77,26 @@ __device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plan
     }
     const int ja = max(0, -v0), jb = min(cols, Wi - v0);  // in-image columns, tile coordinates
     if (ja >= jb) {
-        for (int i = tid; i < rows * cols; i += nt) tile[(i / cols) * pitch + i % cols] = 0.f;
+        for (int i = tid; i < nr * cols; i += nt) tile[(i / cols) * rstep * pitch + i % cols] = 0.f;
         return;
     }
+    // staged rows inside the image: k in [ka, kb)  (h0 + k * rstep in [0, Hi))
+    const int ka = min(nr, (max(0, -h0) + rstep - 1) / rstep);
+    const int kb = max(ka, min(nr, (Hi - h0 + rstep - 1) / rstep));
     {  // zero halo (no loads): whole rows outside the image, the side columns of the others
         const int side = ja + (cols - jb);
-        for (int i = tid; i < rows * side; i += nt) {
-            const int r = i / side, k = i - r * side;
-            const int h = h0 + r;
-            if (h < 0 || h >= Hi) continue;
-            tile[r * pitch + (k < ja ? k : jb + (k - ja))] = 0.f;
+        for (int i = tid; i < (kb - ka) * side; i += nt) {
+            const int k = ka + i / side, m = i % side;
+            tile[k * rstep * pitch + (m < ja ? m : jb + (m - ja))] = 0.f;
         }
-        const int ra0 = max(0, -h0), rb0 = max(ra0, min(rows, Hi - h0));
-        const int nout = ra0 + (rows - rb0);  // rows outside the image: [0, ra0) and [rb0, rows)
+        const int nout = ka + (nr - kb);  // staged rows outside the image: [0, ka) and [kb, nr)
         for (int i = tid; i < nout * cols; i += nt) {
-            const int k = i / cols, r = k < ra0 ? k : rb0 + (k - ra0);
-            tile[r * pitch + (i - k * cols)] = 0.f;
+            const int o = i / cols, k = o < ka ? o : kb + (o - ka);
+            tile[k * rstep * pitch + (i - o * cols)] = 0.f;
         }
     }
-    const int ra = max(0, -h0), rb = min(rows, Hi - h0);  // in-image rows
     const int ma = (v0 + ja) / V, mb = (v0 + jb + V - 1) / V;  // 16-byte chunks covering the columns
-    const int nm = mb - ma, total = (rb - ra) * nm;
+    const int nm = mb - ma, total = (kb - ka) * nm;
     constexpr int U = 4;  // four independent 16-byte loads in flight per thread
     for (int i0 = tid; i0 < total; i0 += U * nt) {
         uint4 u[U];
@@ -104,14 +105,14 @@ __device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plan
             const int i = i0 + q * nt;
             if (i < total) {
                 const int rr = i / nm, m = ma + (i - rr * nm);
-                u[q] = __ldg(reinterpret_cast<const uint4 *>(plane + (size_t)(h0 + ra + rr) * Wi) + m);
+                u[q] = __ldg(reinterpret_cast<const uint4 *>(plane + (size_t)(h0 + (ka + rr) * rstep) * Wi) + m);
             }
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const int i = i0 + q * nt;
             if (i >= total) break;
-            const int rr = i / nm, m = ma + (i - rr * nm), r = ra + rr;
+            const int rr = i / nm, m = ma + (i - rr * nm), r = (ka + rr) * rstep;
             const T *e = reinterpret_cast<const T *>(&u[q]);
 #pragma unroll
             for (int k = 0; k < V; ++k) {
@@ -149,6 +150,7 @@ struct StencilArgs {
     int minDH, maxDH, minDW;
     int band, bands;
     int tileRows, tileCols, pitch;
+    int rstep;  // Stencil::rstep
 };
 
 // out[p][q] = sum_e in[str*p + dh_e][str*q + dw_e] * coef_e * w_{k_e}, one CTA per (plane, band of output rows)
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     const T *in = static_cast<const T *>(a.in) + (size_t)plane * a.Hi * a.Wi;
     const int h0 = a.str * p0 + a.minDH;
     const int rows = a.str * (nrows - 1) + 1 + (a.maxDH - a.minDH);
-    stage_tile<T>(tile, a.pitch, in, a.Hi, a.Wi, h0, rows, a.minDW, a.tileCols);
+    stage_tile<T>(tile, a.pitch, in, a.Hi, a.Wi, h0, rows, a.minDW, a.tileCols, a.rstep);
     __syncthreads();
     T *out = static_cast<T *>(a.out) + (size_t)plane * a.Ho * a.Wo;
     const int qg = (a.Wo + 3) >> 2;
@@ -314,6 +316,7 @@ struct BwdWArgs {
     int minOH, maxOH, minOW;
     int band, bands;
     int tileRows, tileCols, pitch;
+    int rstep;  // Stencil::rstep of the forward geometry
 };
 
 // NV per-lane values -> lane L (< NV) ends with the warp sum of v[L] (NV a power of two <= 32)
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(kThreads) bwd_weight_generic_kernel(BwdWArgs a
     const T *dy = static_cast<const T *>(a.dy) + (size_t)plane * a.P * a.Q + (size_t)p0 * a.Q;
     const int h0 = a.str * p0 + a.minOH;
     const int rows = a.str * (nrows - 1) + 1 + (a.maxOH - a.minOH);
-    stage_tile<T>(tile, a.pitch, x, a.H, a.W, h0, rows, a.minOW, a.tileCols);
+    stage_tile<T>(tile, a.pitch, x, a.H, a.W, h0, rows, a.minOW, a.tileCols, a.rstep);
     stage_tile<T>(sdy, a.Q, dy - (size_t)p0 * a.Q, a.P, a.Q, p0, nrows, 0, a.Q);
     __syncthreads();
     float *ws = a.ws + (size_t)blockIdx.x * a.K;
@@ -460,7 +463,7 @@ o1d_status generic_stencil(const o1d_plan *pl, const Stencil &st, int band, cons
     a.in = in; a.w = w; a.out = out; a.dh = st.d_dh; a.dw = st.d_dw; a.ek = pl->d_ek; a.coef = pl->d_coef;
     a.C = pl->d.C; a.Hi = st.Hi; a.Wi = st.Wi; a.Ho = st.Ho; a.Wo = st.Wo; a.str = st.str; a.K = pl->d.K; a.KE = st.KE;
     a.minDH = st.minDH; a.maxDH = st.maxDH; a.minDW = st.minDW;
-    a.band = band; a.bands = (st.Ho + band - 1) / band;
+    a.band = band; a.bands = (st.Ho + band - 1) / band; a.rstep = st.rstep;
     tile_geometry(st, band, &a.tileRows, &a.tileCols, &a.pitch);
     const size_t smem = stencil_smem(st, band, 0);
     const long grid = (long)pl->d.N * pl->d.C * a.bands;
@@ -526,7 +529,7 @@ o1d_status generic_bwd_weight(const o1d_plan *pl, const void *x, const void *dy,
     a.x = x; a.dy = dy; a.ws = ws; a.oh = pl->d_oh; a.ow = pl->d_ow;
     a.C = d.C; a.H = d.H; a.W = d.W; a.P = pl->P; a.Q = pl->Q; a.str = d.stride; a.K = pl->KE;
     a.minOH = st.minDH; a.maxOH = st.maxDH; a.minOW = st.minDW;
-    a.band = pl->bw_band; a.bands = pl->bw_bands;
+    a.band = pl->bw_band; a.bands = pl->bw_bands; a.rstep = st.rstep;
     tile_geometry(st, a.band, &a.tileRows, &a.tileCols, &a.pitch);
     const size_t smem = sizeof(float) * ((size_t)a.tileRows * a.pitch + (size_t)a.band * a.Q + pl->KE);
     const long grid = (long)d.N * d.C * a.bands;

@@ -391,6 +391,11 @@ o1d_status o1d_plan_create(const o1d_desc *d, const double *angles_deg, o1d_plan
                       pl->d_oh, pl->d_ow};
     pl->bwd_in = Stencil{pl->P, pl->Q, d->H, d->W, 1, KE, -pl->maxOH, -pl->minOH, -pl->maxOW, -pl->minOW,
                          pl->d_noh, pl->d_now};
+    if (d->stride > 1) {  // only rows str*p + dh are read: skip the others when every dh agrees mod str
+        bool cong = true;
+        for (size_t e = 0; e < pl->eoh.size() && cong; ++e) cong = ((pl->eoh[e] - pl->minOH) % d->stride) == 0;
+        if (cong) pl->fwd.rstep = d->stride;
+    }
     pl->fwd_band = generic_band_rows(pl, pl->fwd, 0);
     pl->bi_band = d->stride == 1 ? generic_band_rows(pl, pl->bwd_in, 0) : 1;
     pl->bw_band = generic_band_rows(pl, pl->fwd, 1);

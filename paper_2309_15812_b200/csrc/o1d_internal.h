@@ -30,6 +30,9 @@ struct Stencil {
     int Hi, Wi, Ho, Wo, str, KE;
     int minDH, maxDH, minDW, maxDW;  // over all channels
     const int16_t *d_dh, *d_dw;      // device [C][KE]
+    // input rows the taps can reach are every rstep-th row of a tile (str > 1 and every dh congruent
+    // mod str, e.g. the stem's horizontal stride-2 layer): the others are never staged
+    int rstep = 1;
 };
 
 struct SpecSet;  // JIT-specialised kernels for one plan (o1d_spec.cpp)
