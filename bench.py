@@ -626,7 +626,7 @@ def run_ours(args):
         "gpu_launches": launches, "clocks": ck, "e2e": e2e,
     }
     line.update(extra)
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the oracle baseline: rank 0 at N=1 only
         try:
             line["cpu_baseline"] = cpu_baseline(wl, args.dtype)
         except Exception as ex:  # pragma: no cover
@@ -636,7 +636,8 @@ def run_ours(args):
         out = subprocess.run([sys.executable, os.path.abspath(__file__)] + extra_args, capture_output=True, text=True,
                              timeout=timeout, env={**os.environ, "WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": str(local)})
         return json.loads(out.stdout.strip().splitlines()[-1])
-    if rank == 0 and not args.no_extra and args.dtype == "f32":
+    # single-GPU extras (bf16, bilinear, the model step) on the N=1 line only: the scaling runs stay short
+    if rank == 0 and world == 1 and not args.no_extra and args.dtype == "f32":
         common = ["--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu", "--no-extra",
                   "--flags", str(args.flags)]
         for key, ex in (("bf16", ["--dtype", "bf16"]), ("bilinear", ["--disc", "bilinear"])):
