@@ -123,23 +123,6 @@ __device__ __forceinline__ void stage_tile(float *tile, int pitch, const T *plan
     }
 }
 
-// four consecutive outputs of a row, packed into one 8- or 16-byte store when aligned
-template <typename T>
-__device__ __forceinline__ void store4(T *o, const float (&acc)[4], int nvalid) {
-    if (nvalid == 4 && (reinterpret_cast<uintptr_t>(o) & (4 * sizeof(T) - 1)) == 0) {
-        if constexpr (sizeof(T) == 4) {
-            *reinterpret_cast<float4 *>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        } else {
-            T v[4] = {to_act<T>(acc[0]), to_act<T>(acc[1]), to_act<T>(acc[2]), to_act<T>(acc[3])};
-            *reinterpret_cast<uint2 *>(o) = *reinterpret_cast<const uint2 *>(v);
-        }
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (j < nvalid) o[j] = to_act<T>(acc[j]);
-}
-
 struct StencilArgs {
     const void *in;
     const float *w;
@@ -179,7 +162,12 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
     stage_tile<T>(tile, a.pitch, in, a.Hi, a.Wi, h0, rows, a.minDW, a.tileCols, a.rstep);
     __syncthreads();
     T *out = static_cast<T *>(a.out) + (size_t)plane * a.Ho * a.Wo;
-    const int qg = (a.Wo + 3) >> 2;
+    // a warp computes 32 consecutive outputs of a row, 4 times 32 apart (q = qc + 32 j): the lanes read
+    // consecutive shared-memory words (the round-2 map of 4 consecutive outputs per thread put lanes 4
+    // words apart: 4-way bank conflicts, x str for strided planes -- ncu: 74% of the shared-memory
+    // wavefronts were conflicts at the stem's 112^2 layer)
+    // J outputs per lane (J = 1..4, as many 32-wide columns as the row needs), chunks of 32 J outputs
+    const int J = min(4, (a.Wo + 31) >> 5), cw = 32 * J, nch = (a.Wo + cw - 1) / cw;
     int roff[KC > 0 ? KC : 1];
     float rw[KC > 0 ? KC : 1];
     if constexpr (KC > 0) {
@@ -189,33 +177,40 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
             rw[k] = k < a.KE ? wk[k] : 0.f;
         }
     }
-    for (int g = tid; g < nrows * qg; g += blockDim.x) {
-        const int pr = g / qg, q0 = (g - pr * qg) * 4;
-        const float *base = tile + pr * a.str * a.pitch + q0 * a.str;
+    for (int g = tid; g < nrows * nch * 32; g += blockDim.x) {  // blockDim.x is a multiple of 32
+        const int t = g >> 5, pr = nch == 1 ? t : t / nch, qc = (t - pr * nch) * cw + (g & 31);
+        const float *row = tile + pr * a.str * a.pitch;
+        // outputs past the row (last chunk) read in-row columns and are not stored
+        const int lim = min(a.Wo - 1, qc - (g & 31) + cw - 1);  // this chunk's last in-row output
+        const float *b0 = row + min(qc, lim) * a.str, *b1 = row + min(qc + 32, lim) * a.str;
+        const float *b2 = row + min(qc + 64, lim) * a.str, *b3 = row + min(qc + 96, lim) * a.str;
         float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
         if constexpr (KC > 0) {
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 if (k >= a.KE) break;  // (no padding taps: 0 * inf would leak a non-finite input)
-                const float *s = base + roff[k];
+                const int o = roff[k];
                 const float wv = rw[k];
-                acc0 = fmaf(s[0], wv, acc0);
-                acc1 = fmaf(s[a.str], wv, acc1);
-                acc2 = fmaf(s[2 * a.str], wv, acc2);
-                acc3 = fmaf(s[3 * a.str], wv, acc3);
+                acc0 = fmaf(b0[o], wv, acc0);
+                if (J > 1) acc1 = fmaf(b1[o], wv, acc1);
+                if (J > 2) acc2 = fmaf(b2[o], wv, acc2);
+                if (J > 3) acc3 = fmaf(b3[o], wv, acc3);
             }
         } else {
             for (int k = 0; k < a.KE; ++k) {
-                const float *s = base + toff[k];
+                const int o = toff[k];
                 const float wv = wk[k];
-                acc0 = fmaf(s[0], wv, acc0);
-                acc1 = fmaf(s[a.str], wv, acc1);
-                acc2 = fmaf(s[2 * a.str], wv, acc2);
-                acc3 = fmaf(s[3 * a.str], wv, acc3);
+                acc0 = fmaf(b0[o], wv, acc0);
+                if (J > 1) acc1 = fmaf(b1[o], wv, acc1);
+                if (J > 2) acc2 = fmaf(b2[o], wv, acc2);
+                if (J > 3) acc3 = fmaf(b3[o], wv, acc3);
             }
         }
-        const float acc[4] = {acc0, acc1, acc2, acc3};
-        store4<T>(out + (size_t)(p0 + pr) * a.Wo + q0, acc, min(4, a.Wo - q0));
+        T *orow = out + (size_t)(p0 + pr) * a.Wo;
+        if (qc <= lim) orow[qc] = to_act<T>(acc0);
+        if (J > 1 && qc + 32 <= lim) orow[qc + 32] = to_act<T>(acc1);
+        if (J > 2 && qc + 64 <= lim) orow[qc + 64] = to_act<T>(acc2);
+        if (J > 3 && qc + 96 <= lim) orow[qc + 96] = to_act<T>(acc3);
     }
 }
 
@@ -287,9 +282,11 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdIn
     stage_tile<T>(tile, a.pitch, dy, a.P, a.Q, a0, a.tileRows, b0, a.tileCols);
     __syncthreads();
     T *dx = static_cast<T *>(a.dx) + (size_t)plane * a.H * a.W;
-    const int qg = (a.W + 3) >> 2;
-    for (int g = tid; g < nrows * qg; g += blockDim.x) {
-        const int hr = g / qg, w0 = (g - hr * qg) * 4, h = hb + hr;
+    // 32 consecutive dx outputs of a row per warp, 4 times 32 apart (conflict-free shared reads, see
+    // stencil_generic_kernel)
+    const int nch = (a.W + 127) >> 7;
+    for (int g = tid; g < nrows * nch * 32; g += blockDim.x) {
+        const int t = g >> 5, hr = t / nch, wc = (t - hr * nch) * 128 + (g & 31), h = hb + hr;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int e = 0; e < a.KE; ++e) {
             const int i = c * a.KE + e;
@@ -300,11 +297,14 @@ __global__ void __launch_bounds__(kThreads) bwd_input_strided_tiled_kernel(BwdIn
             const int ow = a.ow[i];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int cn = w0 + j - ow - s * b0;
+                const int cn = wc + 32 * j - ow - s * b0;
                 if (cn >= 0 && cn % s == 0 && (cn / s) < a.tileCols) acc[j] = fmaf(row[cn / s], wv, acc[j]);
             }
         }
-        store4<T>(dx + (size_t)h * a.W + w0, acc, min(4, a.W - w0));
+        T *drow = dx + (size_t)h * a.W;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (wc + 32 * j < a.W) drow[wc + 32 * j] = to_act<T>(acc[j]);
     }
 }
 
