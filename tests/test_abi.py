@@ -191,3 +191,47 @@ def test_small_plane_source_compiles_for_sm100a(tmp_path, pass_id, dtype):
     sass = subprocess.run(["cuobjdump", "-sass", str(tmp_path / "s.cubin")], capture_output=True, text=True).stdout
     assert "FFMA2" in sass
     assert ("UTMALDG" in sass) == (dtype == "f32") and ("LDGSTS.E" in sass) == (dtype != "f32" or pass_id <= 1)
+
+
+@pytest.mark.parametrize("pass_id", [0, 2])
+def test_flat_16bit_source_compiles_for_sm100a(tmp_path, pass_id):
+    """16-bit planes whose rows are not 16-byte multiples (ConvNeXt stage 2: 28 x 2 B) get the
+    specialised kernels through flat TMA views (planes as rows of 8 elements); 30-wide planes (rows of
+    4-element units do not fit) stay on the generic kernels."""
+    import shutil
+    import subprocess
+    import torch
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    src = B.spec_source(4, 16, 28, 28, 31, T.direction_angles(8, 16, "cycled"), pass_id, dtype=torch.bfloat16)
+    if pass_id == 0:
+        assert "row0 * 14 / 4" in src  # band store at element row0 * 28 / 8 of the flat view
+    f = tmp_path / f"f{pass_id}.cu"
+    f.write_text(src)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-o", str(tmp_path / "f.cubin"),
+                        str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    with pytest.raises(B.O1DError):
+        B.spec_source(4, 16, 30, 30, 31, T.direction_angles(8, 16, "cycled"), pass_id, dtype=torch.bfloat16)
+
+
+def test_wgrad_pair_step_selection(monkeypatch):
+    """backward_weight packs tap pairs along the step with the fewest generated FMA instructions
+    (16 candidates): the same FMA count as the round-1 candidate set (4 steps), never more
+    instructions, strictly fewer for the near-22.5 deg tables of D=8."""
+    import re
+
+    def counts(n):
+        monkeypatch.setenv("O1D_PPSTEPS", str(n))
+        src = B.spec_source(2, 16, 56, 56, 31, T.direction_angles(8, 16, "cycled"), 2)
+        out = []
+        for body in re.split(r"\n    case \d+: \{", src)[1:]:
+            body = body.split("break;")[0]
+            f2, f1 = body.count("ffma2("), body.count("fmaf(")
+            out.append((2 * f2 + f1, f2 + f1))
+        return out
+
+    c16, c4 = counts(16), counts(4)
+    assert len(c16) == len(c4) == 8
+    for (fma16, ins16), (fma4, ins4) in zip(c16, c4):
+        assert fma16 == fma4 and ins16 <= ins4
+    assert sum(i for _, i in c16) < sum(i for _, i in c4)
