@@ -105,6 +105,9 @@ typedef struct o1d_plan o1d_plan;
  * reduced mod 360 deg exactly; at the Niven angles (sin or cos in {0,+-1/2,+-1})
  * the product is evaluated exactly, elsewhere it is irrational and its floor is
  * taken from f64 trig, re-evaluated in binary128 when within 1e-9 of an integer.
+ * This is NOT SPEC's rule (f64 trig, snapped only at multiples of 90 deg): the two
+ * differ on the 30-degree family, e.g. theta = 30, k - pad = -2 gives floor(2 * 0.49999999999999994)
+ * = 0 under SPEC's rule and the exact floor(1) = 1 here (reading R3).
  * angles_deg: host [C] (degrees, any finite real).  oh, ow: host [C][K] outputs.
  * pad: any negative value => floor(K/2); otherwise a finite real |pad| <= 4096 (k - pad
  * is then a binary double, so the same exactness argument holds).  Pure host
