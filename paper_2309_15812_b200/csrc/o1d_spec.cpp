@@ -36,6 +36,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -2287,6 +2289,47 @@ const char *kSrcName[kPasses] = {"o1d_fwd.cu", "o1d_bwd_in.cu", "o1d_wgrad.cu", 
 
 // compile (or take from the module cache) and load the modules of passes `which`; sets
 // launch geometry.  *all_hit: every module came from the cache.
+// On-disk cubin cache (across processes): NVRTC takes seconds per generated pass, and a model builds
+// one plan per distinct layer shape.  Key = FNV-1a 64 of (source, compile options); files
+// <dir>/o1d_<key>.cubin (+ .log: the ptxas report).  dir = $O1D_CACHE_DIR, else $HOME/.cache/oriented1d;
+// O1D_DISK_CACHE=0 disables it.  Writes go to a temporary name and are renamed into place, so readers
+// never see a partial file; an entry that fails to load is recompiled.
+std::string disk_cache_path(const std::string &src) {
+    if (env_int("O1D_DISK_CACHE", 1) == 0) return std::string();
+    std::string dir;
+    if (const char *d = getenv("O1D_CACHE_DIR")) dir = d;
+    else if (const char *h = getenv("HOME")) dir = std::string(h) + "/.cache/oriented1d";
+    if (dir.empty()) return std::string();
+    mkdir((dir.substr(0, dir.rfind('/'))).c_str(), 0755);
+    mkdir(dir.c_str(), 0755);
+    unsigned long long h = 1469598103934665603ull;
+    const std::string key = src + "\n// sm_100a -std=c++17 -lineinfo -DNDEBUG v1";
+    for (unsigned char ch : key) h = (h ^ ch) * 1099511628211ull;
+    char name[64];
+    snprintf(name, sizeof name, "/o1d_%016llx", h);
+    return dir + name;
+}
+bool read_file(const std::string &path, std::string *out) {
+    FILE *f = fopen(path.c_str(), "rb");
+    if (!f) return false;
+    std::string d;
+    char buf[1 << 16];
+    size_t n;
+    while ((n = fread(buf, 1, sizeof buf, f)) > 0) d.append(buf, n);
+    fclose(f);
+    *out = d;
+    return !d.empty();
+}
+void write_file_atomic(const std::string &path, const char *data, size_t n) {
+    const std::string tmp = path + ".tmp" + std::to_string((long)getpid()) + "_" +
+                            std::to_string((unsigned long)std::hash<std::thread::id>()(std::this_thread::get_id()));
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool ok = fwrite(data, 1, n, f) == n;
+    if (fclose(f) == 0 && ok) rename(tmp.c_str(), path.c_str());
+    else unlink(tmp.c_str());
+}
+
 o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::string *src, int device, long planes,
                        bool *all_hit) {
     Driver &dr = drv();
@@ -2299,10 +2342,29 @@ o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::st
         sp->mod[i] = cache_get(device, src[i]);
         if (!sp->mod[i]) need[i] = true, *all_hit = false;
     }
+    std::string dpath[kPasses];
+    bool from_disk[kPasses] = {false, false, false, false};
+    for (int i = 0; i < kPasses; ++i) {
+        if (!need[i]) continue;
+        dpath[i] = disk_cache_path(src[i]);
+        std::string cb, lg;
+        if (!dpath[i].empty() && read_file(dpath[i] + ".cubin", &cb) && read_file(dpath[i] + ".log", &lg)) {
+            cubin[i].assign(cb.begin(), cb.end());
+            logs[i] = lg;
+            from_disk[i] = true;
+        }
+    }
+    auto compile = [&](int i) {
+        ok[i] = compile_cubin(src[i], kSrcName[i], &cubin[i], &logs[i]);
+        if (ok[i] && !dpath[i].empty()) {
+            write_file_atomic(dpath[i] + ".cubin", cubin[i].data(), cubin[i].size());
+            write_file_atomic(dpath[i] + ".log", logs[i].data(), logs[i].size());
+        }
+    };
     {
         std::vector<std::thread> th;
         for (int i = 0; i < kPasses; ++i)
-            if (need[i]) th.emplace_back([&, i] { ok[i] = compile_cubin(src[i], kSrcName[i], &cubin[i], &logs[i]); });
+            if (need[i] && !from_disk[i]) th.emplace_back([&, i] { compile(i); });
         for (auto &t : th) t.join();
     }
     for (int i = 0; i < kPasses; ++i)
@@ -2312,6 +2374,12 @@ o1d_status load_passes(SpecSet *sp, const std::vector<int> &which, const std::st
         auto m = std::make_shared<Mod>();
         CUresult r = dr.ctxGetCurrent(&m->ctx);
         if (r == CUDA_SUCCESS) r = dr.moduleLoadData(&m->mod, cubin[i].data());
+        if (r != CUDA_SUCCESS && from_disk[i]) {  // a stale or damaged cache entry: compile afresh
+            from_disk[i] = false;
+            compile(i);
+            if (!ok[i]) return fail(O1D_JIT_ERROR, std::string("NVRTC failed for ") + kSrcName[i] + ":\n" + logs[i].substr(0, 4000));
+            r = dr.moduleLoadData(&m->mod, cubin[i].data());
+        }
         if (r == CUDA_SUCCESS) r = dr.moduleGetFunction(&m->fn, m->mod, sp->small ? "o1d_small" : kFnName[i]);
         if (r == CUDA_SUCCESS && i >= 2) r = dr.moduleGetFunction(&m->fin, m->mod, "o1d_wgrad_finalize");
         if (r != CUDA_SUCCESS) return fail(O1D_CUDA_ERROR, std::string("loading specialised kernel: ") + cu_err(r));

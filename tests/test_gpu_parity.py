@@ -630,3 +630,45 @@ def test_flat_16bit_planes(shape, dtype):
     angles = B.direction_angles(8, C, assign)
     plan, errs = run_case(N, C, H, W, K, angles, dtype=dtype, check_det=True, expect="spec")
     assert "spec-small" not in plan.describe()
+
+
+def test_disk_cubin_cache(tmp_path):
+    """The on-disk cubin cache: a second process building the same plan loads the compiled modules from
+    O1D_CACHE_DIR instead of running NVRTC (plan creation several times faster) and computes bitwise
+    the same outputs; a damaged cache entry is recompiled."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2309_15812_b200 import binding as B, inputs
+ang = B.direction_angles(8, 16, "cycled")
+plan = B.Plan(2, 16, 56, 56, 31, ang, device="cuda:0")
+x = torch.from_numpy(inputs.activation((2, 16, 56, 56), 0)).cuda()
+w = torch.from_numpy(inputs.weights(16, 31, 1)).cuda()
+y = B.forward(plan, x, w)
+dW = B.backward_weight(plan, x, y)
+torch.cuda.synchronize()
+print(json.dumps({"ms": plan.stats()[0], "y": float(y.double().sum()), "dW": dW.double().cpu().numpy().tolist()}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "O1D_CACHE_DIR": str(tmp_path / "cache")}
+
+    def run():
+        out = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, env=env, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads(out.stdout.strip().splitlines()[-1])
+
+    first = run()
+    files = sorted(os.listdir(tmp_path / "cache"))
+    assert any(f.endswith(".cubin") for f in files) and any(f.endswith(".log") for f in files), files
+    second = run()
+    assert second["y"] == first["y"] and second["dW"] == first["dW"]
+    assert second["ms"] < first["ms"] / 3, (first["ms"], second["ms"])
+    for f in files:  # damage every cubin: the next process must recompile and still be right
+        if f.endswith(".cubin"):
+            (tmp_path / "cache" / f).write_bytes(b"not a cubin")
+    third = run()
+    assert third["y"] == first["y"] and third["dW"] == first["dW"]
