@@ -111,6 +111,28 @@ def algorithmic_fmas(wl):
     return wl.N * wl.C * wl.H * wl.W * wl.K  # dense taps per output (zero padding is free in smem)
 
 
+def bilinear_fmas(wl, angles):
+    """FMAs per pass of the bilinear discretisation (reading R14): every output takes each
+    DISTINCT neighbour offset of its channel's weighted taps once (the four corners of each tap with a
+    non-zero weight, coincident corners of consecutive taps merged) -- from the library's host tap
+    generator (o1d_make_bilinear), the same count the generated kernels hold (31 / 71 / 67 / 71 per
+    channel at K=31 for 0 / 22.5 / 45 / 67.5 deg)."""
+    import numpy as np
+
+    from paper_2309_15812_b200 import binding as B
+    h0, w0, fa, fb = B.make_bilinear(wl.K, angles)
+    tot = 0
+    for c in range(h0.shape[0]):
+        offs = set()
+        for k in range(wl.K):
+            for dh, wa in ((0, 1 - fa[c, k]), (1, fa[c, k])):
+                for dw, wb in ((0, 1 - fb[c, k]), (1, fb[c, k])):
+                    if np.float32(wa * wb) != 0:
+                        offs.add((int(h0[c, k]) + dh, int(w0[c, k]) + dw))
+        tot += len(offs)
+    return wl.N * wl.H * wl.W * tot
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -531,7 +553,8 @@ def run_ours(args):
     launches = (plan.launches_per_call(0) + (plan.launches_per_call(3) if fused_step else
                                             plan.launches_per_call(1) + plan.launches_per_call(2))) * args.steps
     fpk, fpk_src = ffma_peak()
-    fmas_pass = algorithmic_fmas(wl)
+    # bilinear: four weighted corners per tap, the arithmetic intensity is past the FFMA/HBM ridge
+    fmas_pass = bilinear_fmas(wl, angles) if args.disc == "bilinear" else algorithmic_fmas(wl)
 
     # end to end through the C ABI with pinned HOST buffers (H2D + 3 passes + D2H per step)
     e2e = None
@@ -604,12 +627,13 @@ def run_ours(args):
             extra["comparator"] = {"what": f"torch conv2d depthwise {wl.K}x{wl.K} fwd+bwd (cuDNN), same shape",
                                    "ms_per_step": t0k.elapsed_time(t1k) / nk, "ours_ms_per_step": ms_step,
                                    "ours_speedup": (t0k.elapsed_time(t1k) / nk) / ms_step}
-    bound_alu = args.dtype != "f32"
+    bound_alu = args.dtype != "f32" or args.disc == "bilinear"
     roof = {"kernel": dom, "unit": "GB/s", "algorithmic_bytes_per_launch": ab[dom], "peak_source": peak_src,
             "timing": "mean launch duration, back-to-back launches of the kernel (see per_pass_timing)",
             "frac_isolated": ab[dom] / (per_pass_iso[dom] / args.steps * 1e-3) / 1e9 / peak}
     if bound_alu:
-        # 16-bit activations: arithmetic intensity 15.5 flop/B > the FFMA/HBM ridge -> FFMA bound
+        # 16-bit activations (15.5 flop/B) and the bilinear taps (~31 flop/B at fp32, 60 distinct
+        # offsets per output): past the FFMA/HBM ridge -> FFMA bound
         fl = (2 if dom == "backward_fused" else 1) * 2 * fmas_pass / (dom_ms * 1e-3) / 1e12
         roof.update({"bound": "alu", "achieved": fl, "peak": fpk, "unit": "TFLOP/s", "frac": fl / fpk,
                      "peak_source": fpk_src, "hbm_gbs": achieved, "hbm_frac": achieved / peak, "traffic": None})
