@@ -1005,13 +1005,14 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
     const size_t bytes = (cvt ? 0 : (size_t)L.hin * L.pitch * 4) + (wgrad ? (size_t)L.dyp * L.dyrows * es : 0) +
                          (fused && !cvt ? (size_t)L.hin2 * L.pitch2 * 4 : 0);
     const int PQ = (P + L.NPROD - 1) / L.NPROD;  // pairs per producer warp
-    const int PREF = 2;                          // single-item scheduler atomics in flight
+    // single-item scheduler atomics in flight (0: claim when a slot frees)
+    const int PREF = std::max(0, env_int("O1D_PREF", 0)), PA = std::max(1, PREF);
     os << "  if (warp < " << L.NPROD << ") {\n"
        << "    const int pw = warp;\n"
        << "    int tcur = 0, tried = 0;\n"
        << "    const u64 pol = policy_evict_first();\n"
        << "    const int nper = p.nlen > 0 ? p.nlen : p.N;\n"
-       << "    unsigned lo = 0, pf[" << PREF << "];   // the first P_NB items come in one batch (fills the ring without round trips)\n"
+       << "    unsigned lo = 0, pf[" << PA << "];   // the first P_NB items come in one batch (fills the ring without round trips)\n"
        << "    // the scheduler counters of this launch slot were last touched 64 launches ago: the\n"
        << "    // first atomics run before griddepcontrol.wait (only x / dy / w may come from the predecessor)\n"
        << "    if (lane == 0) {\n"
@@ -1020,6 +1021,7 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "      lo = atomicAdd(p.sched + tcur * CS, " << PQ * NB << "u);\n"
        << "#pragma unroll\n"
        << "      for (int k = 0; k < " << PREF << "; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << "      (void)pf;\n"
        << "    }\n"
        << "    if (!p.nowait) pdl_wait();\n"
        << "    int jq[" << PQ << "];   // items issued per served pair (-1: end marker sent)\n"
@@ -1044,17 +1046,19 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "            item = (tcur << 22) | (int)(lo + bat++);\n"
        << "          } else {\n"
        << "            bat = " << PQ * NB << ";   // the batch is exhausted: every later item comes from pf\n"
-       << "            const unsigned v = pf[0];\n"
-       << "#pragma unroll\n"
-       << "            for (int k = 0; k + 1 < " << PREF << "; ++k) pf[k] = pf[k + 1];\n"
-       << "            const int t0 = tcur;\n"
-       << "            item = sched_resolve(p.sched, tcur, v, tried, nper);\n"
-       << "            if (tcur != t0) {   // moved to another table: the prefetched indices belong to the old one\n"
-       << "#pragma unroll\n"
-       << "              for (int k = 0; k < " << PREF << "; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-       << "            } else {\n"
-       << "              pf[" << PREF - 1 << "] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-       << "            }\n"
+       << (PREF == 0 ? "            const unsigned v = atomicAdd(p.sched + tcur * CS, 1u);\n"
+                         "            item = sched_resolve(p.sched, tcur, v, tried, nper);\n"
+                       : "            const unsigned v = pf[0];\n"
+                         "#pragma unroll\n"
+                         "            for (int k = 0; k + 1 < " + std::to_string(PREF) + "; ++k) pf[k] = pf[k + 1];\n"
+                         "            const int t0 = tcur;\n"
+                         "            item = sched_resolve(p.sched, tcur, v, tried, nper);\n"
+                         "            if (tcur != t0) {   // moved to another table: the prefetched indices belong to the old one\n"
+                         "#pragma unroll\n"
+                         "              for (int k = 0; k < " + std::to_string(PREF) + "; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                         "            } else {\n"
+                         "              pf[" + std::to_string(PREF - 1) + "] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                         "            }\n")
        << "          }\n"
        << "        }\n"
        << "        item = __shfl_sync(0xffffffffu, item, 0);\n"
@@ -1153,7 +1157,7 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
     const int Win = x.Wo;  // stride 1: input width = output width
     const size_t raw = (size_t)L.hin * Win * es;
     (void)es;
-    const int PREF = 2;
+    const int PREF = std::max(0, std::min(2, env_int("O1D_PREF", 0))), PA = std::max(1, PREF);  // see emit_producer
     auto claim = [&](const char *var) {
         os << "      {\n"
            << "        int it_ = -1;\n"
@@ -1161,18 +1165,21 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
            << "          if (bat < " << NB << " && lo + bat < (unsigned)(nch_of(tcur) * nper)) {\n"
            << "            it_ = (tcur << 22) | (int)(lo + bat++);\n"
            << "          } else {\n"
-           << "            bat = " << NB << ";\n"
-           << "            const unsigned v = pf[0];\n"
-           << "            pf[0] = pf[1];\n"
-           << "            const int t0 = tcur;\n"
-           << "            it_ = sched_resolve(p.sched, tcur, v, tried, nper);\n"
-           << "            if (tcur != t0) {\n"
-           << "              pf[0] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-           << "              pf[1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-           << "            } else {\n"
-           << "              pf[1] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-           << "            }\n"
-           << "          }\n"
+           << "            bat = " << NB << ";\n";
+        if (PREF == 0) {
+            os << "            it_ = sched_resolve(p.sched, tcur, atomicAdd(p.sched + tcur * CS, 1u), tried, nper);\n";
+        } else {
+            os << "            const unsigned v = pf[0];\n"
+               << "            for (int k = 0; k + 1 < " << PREF << "; ++k) pf[k] = pf[k + 1];\n"
+               << "            const int t0 = tcur;\n"
+               << "            it_ = sched_resolve(p.sched, tcur, v, tried, nper);\n"
+               << "            if (tcur != t0) {\n"
+               << "              for (int k = 0; k < " << PREF << "; ++k) pf[k] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+               << "            } else {\n"
+               << "              pf[" << PREF - 1 << "] = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+               << "            }\n";
+        }
+        os << "          }\n"
            << "        }\n"
            << "        " << var << " = __shfl_sync(0xffffffffu, it_, 0);\n"
            << "      }\n";
@@ -1191,12 +1198,13 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
        << "    const int nper = p.nlen > 0 ? p.nlen : p.N;\n"
        << "    u64* const stfull = full + 40 + q;\n"
        << "    unsigned char* const stage = smem + " << L.off_st << " + q * " << L.stb << ";\n"
-       << "    unsigned lo = 0, pf[" << PREF << "];\n"
+       << "    unsigned lo = 0, pf[" << PA << "];\n"
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = HOME[smid() % NHOME];\n"
        << "      lo = atomicAdd(p.sched + tcur * CS, " << NB << "u);\n"
        << "      for (int k = 0; k < " << PREF << "; ++k) pf[k] = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << "      (void)pf;\n"
        << "    }\n"
        << "    if (!p.nowait) pdl_wait();\n"
        << "    int nxt;\n";
