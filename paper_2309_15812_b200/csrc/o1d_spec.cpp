@@ -1046,8 +1046,8 @@ void emit_producer(std::ostringstream &os, const Ctx &x, const Lay &L, int pass,
        << "            item = (tcur << 22) | (int)(lo + bat++);\n"
        << "          } else {\n"
        << "            bat = " << PQ * NB << ";   // the batch is exhausted: every later item comes from pf\n"
-       << (PREF == 0 ? "            const unsigned v = atomicAdd(p.sched + tcur * CS, 1u);\n"
-                         "            item = sched_resolve(p.sched, tcur, v, tried, nper);\n"
+       // (tcur < 0: every table is exhausted -- no atomic on a counter before the slot's array)
+       << (PREF == 0 ? "            item = tcur >= 0 ? sched_resolve(p.sched, tcur, atomicAdd(p.sched + tcur * CS, 1u), tried, nper) : -1;\n"
                        : "            const unsigned v = pf[0];\n"
                          "#pragma unroll\n"
                          "            for (int k = 0; k + 1 < " + std::to_string(PREF) + "; ++k) pf[k] = pf[k + 1];\n"
@@ -1167,7 +1167,7 @@ void emit_producer_staged(std::ostringstream &os, const Ctx &x, const Lay &L, in
            << "          } else {\n"
            << "            bat = " << NB << ";\n";
         if (PREF == 0) {
-            os << "            it_ = sched_resolve(p.sched, tcur, atomicAdd(p.sched + tcur * CS, 1u), tried, nper);\n";
+            os << "            it_ = tcur >= 0 ? sched_resolve(p.sched, tcur, atomicAdd(p.sched + tcur * CS, 1u), tried, nper) : -1;\n";
         } else {
             os << "            const unsigned v = pf[0];\n"
                << "            for (int k = 0; k + 1 < " << PREF << "; ++k) pf[k] = pf[k + 1];\n"
@@ -1899,6 +1899,7 @@ void emit_finalize_ne(std::ostringstream &os, int K, const std::string &ne) {
 std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std::vector<Geo> &geo, int Hx, int Wx,
                            std::vector<long> *cost_out) {
     std::ostringstream os;
+    const bool pref = env_int("O1D_PREF", 0) != 0;  // claimed group indices kept in flight (round 2: two)
     emit_header(os, x);
     emit_small_header(os, x.act, L.UPu);
     if (L.tma)
@@ -1946,25 +1947,28 @@ std::string gen_small_pass(const Ctx &x, const SmallLay &L, int pass, const std:
        << "    if (lane == 0) {\n"
        << "      trace_ev(p.trace, 0, -1, trn);\n"
        << "      tcur = HOME[smid() % NHOME];\n"
-       << "      pf0 = atomicAdd(p.sched + tcur * CS, 1u);\n"
-       << "      pf1 = atomicAdd(p.sched + tcur * CS, 1u);\n"
+       << (pref ? "      pf0 = atomicAdd(p.sched + tcur * CS, 1u);\n"
+                  "      pf1 = atomicAdd(p.sched + tcur * CS, 1u);\n" : "")
        << "    }\n"
+       << "    (void)pf0; (void)pf1;\n"
        << "    if (!p.nowait) pdl_wait();\n"
        << "    for (int j = 0;; ++j) {\n"
        << "      const int s = q * " << NB << " + j % " << NB << ";\n"
        << "      if (j >= " << NB << ") mbar_wait(empty + s, ((j / " << NB << ") & 1) ^ 1);\n"
        << "      int item = -1;\n"
        << "      if (lane == 0) {\n"
-       << "        const unsigned v = pf0;\n"
-       << "        pf0 = pf1;\n"
-       << "        const int t0 = tcur;\n"
-       << "        item = sched_resolve(p.sched, tcur, v, tried, G);\n"
-       << "        if (tcur != t0) {\n"
-       << "          pf0 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-       << "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-       << "        } else {\n"
-       << "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
-       << "        }\n"
+       << (pref ? "        const unsigned v = pf0;\n"
+                  "        pf0 = pf1;\n"
+                  "        const int t0 = tcur;\n"
+                  "        item = sched_resolve(p.sched, tcur, v, tried, G);\n"
+                  "        if (tcur != t0) {\n"
+                  "          pf0 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                  "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                  "        } else {\n"
+                  "          pf1 = tcur >= 0 ? atomicAdd(p.sched + tcur * CS, 1u) : 0xffffffffu;\n"
+                  "        }\n"
+                  // claim on demand (O1D_PREF=0, see emit_producer): no claimed-but-unstarted groups at the end
+                : "        item = tcur >= 0 ? sched_resolve(p.sched, tcur, atomicAdd(p.sched + tcur * CS, 1u), tried, G) : -1;\n")
        << "        s_item[s] = item;\n"
        << "        if (item >= 0) trace_ev(p.trace, 1, item, trn);\n"
        << "      }\n"

@@ -672,3 +672,29 @@ print(json.dumps({"ms": plan.stats()[0], "y": float(y.double().sum()), "dW": dW.
             (tmp_path / "cache" / f).write_bytes(b"not a cubin")
     third = run()
     assert third["y"] == first["y"] and third["dW"] == first["dW"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_many_pair_layout_repeated_bitwise(dtype):
+    """Layouts with more than 4 pairs per CTA (28 x 28 planes: one warp per pair, producers serving
+    several pairs) over 150 launches -- every scheduler launch slot reused twice: outputs and dW stay
+    bitwise equal to the first launch (no counter left behind or overwritten by an exhausted producer)."""
+    N, C, H, W, K = 64, 32, 28, 28, 31
+    angles = B.direction_angles(8, C, "cycled")
+    plan = B.Plan(N, C, H, W, K, angles, dtype=dtype, device="cuda:0")
+    assert plan.describe().startswith("spec-v2"), plan.describe()
+    x = torch.from_numpy(inputs.activation((N, C, H, W), 0)).to("cuda:0", dtype)
+    dy = torch.from_numpy(inputs.activation((N, C, H, W), 2)).to("cuda:0", dtype)
+    w = torch.from_numpy(inputs.weights(C, K, 1)).cuda()
+    y0, dx0, dW0 = B.forward(plan, x, w), B.backward_input(plan, dy, w), B.backward_weight(plan, x, dy)
+    y, dx, dW = torch.empty_like(y0), torch.empty_like(dx0), torch.empty_like(dW0)
+    ws = B.workspace(plan)
+    bad = 0
+    for _ in range(150):
+        y.fill_(float("nan")), dx.fill_(float("nan")), dW.fill_(float("nan"))
+        B.forward(plan, x, w, y)
+        B.backward_input(plan, dy, w, dx)
+        B.backward_weight(plan, x, dy, dW, ws)
+        bad += int(not (torch.equal(y, y0) and torch.equal(dx, dx0) and torch.equal(dW, dW0)))
+    torch.cuda.synchronize()
+    assert bad == 0, bad
