@@ -177,6 +177,38 @@ __global__ void __launch_bounds__(kThreads) stencil_generic_kernel(StencilArgs a
             rw[k] = k < a.KE ? wk[k] : 0.f;
         }
     }
+    if (a.Wo <= 32) {
+        // narrow rows (J = 1 would feed one FMA per tap-offset / weight read): 4 consecutive outputs per
+        // thread as in round 2 (bank conflicts, but the tap reads are amortised: 28^2 K=31 270 vs 354 us)
+        const int qg = (a.Wo + 3) >> 2;
+        for (int g = tid; g < nrows * qg; g += blockDim.x) {
+            const int pr = g / qg, q0 = (g - pr * qg) * 4;
+            const float *base = tile + pr * a.str * a.pitch + q0 * a.str;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (KC > 0) {
+#pragma unroll
+                for (int k = 0; k < KC; ++k) {
+                    if (k >= a.KE) break;
+                    const float *s = base + roff[k];
+                    const float wv = rw[k];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = fmaf(s[j * a.str], wv, acc[j]);
+                }
+            } else {
+                for (int k = 0; k < a.KE; ++k) {
+                    const float *s = base + toff[k];
+                    const float wv = wk[k];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = fmaf(s[j * a.str], wv, acc[j]);
+                }
+            }
+            T *orow = out + (size_t)(p0 + pr) * a.Wo + q0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (q0 + j < a.Wo) orow[j] = to_act<T>(acc[j]);
+        }
+        return;
+    }
     for (int g = tid; g < nrows * nch * 32; g += blockDim.x) {  // blockDim.x is a multiple of 32
         const int t = g >> 5, pr = nch == 1 ? t : t / nch, qc = (t - pr * nch) * cw + (g & 31);
         const float *row = tile + pr * a.str * a.pitch;
